@@ -1,0 +1,379 @@
+"""bench.py — ODC hot-path benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl odc|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+Workload "odc_minibatch_comm" (default): one ODC optimizer step (minibatch)
+of the Qwen2.5-1.5B-shaped shard store (28 FSDP units x 46,797,824 elements,
+bf16 params / fp32 grads, block-sharded over the N ranks) driven by the
+LB-Mini plan of the BASELINE long-tail workload (generate_synthetic lognormal
+mu=8 sigma=1.5, 2048 lengths, cap 32768, floored at 512; minibatch 8 per
+rank; budget 32768 tokens). Per microbatch of this rank's LB-Mini queue:
+fetch every unit (forward), fetch every unit again + push its fp32 gradient
+(backward); then the once-per-minibatch barrier and the fused AdamW on the
+owned shards. Every step of it is an sm_100a kernel of libodc.so; the model
+compute between fetch and push is not part of this workload (it is the
+`sft` workload's job).
+
+value  = whole-job fetch+push bytes per second (GB/s), bytes = elements
+         moved x (2 B bf16 fetch, 4 B fp32 push), summed over ranks, over the
+         max-over-ranks device time of K steps (CUDA events, barrier + sync on
+         both sides). Inputs are > L2 (5.2 GB of units per pass), no flush.
+e2e    = the same step through the reference-facing by-value API: each
+         fetched unit is copied to pinned host memory (ShardFabric::gather
+         returns a host vector) and each pushed gradient comes from pinned
+         host memory (scatter_accumulate takes one), copies inside the timed
+         region.
+--impl reference: the reference's own CPU implementation of the same path
+         (ShardFabric<float> from oracle/_ref, built unmodified from
+         /root/reference; the oracle port if _ref is absent) on host cores,
+         one bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P2_BYTES_BF16, P4_BYTES_F32 = 2, 4
+NVLINK_NOMINAL_GBS = 900.0
+METRIC = "tokens/sec at 1/2/4/8 B200 on long-tail seq lengths; fetch/push GB/s vs NVLink"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="odc", choices=["odc", "reference"])
+    ap.add_argument("--workload", default="odc_minibatch_comm", choices=["odc_minibatch_comm"])
+    ap.add_argument("--model", default="qwen2.5-1.5b")
+    ap.add_argument("--push-mode", default="red", choices=["red", "slot"])
+    ap.add_argument("--minibs", type=int, default=8)
+    ap.add_argument("--fetch-ctas", type=int, default=0)
+    ap.add_argument("--push-ctas", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload_lengths():
+    from paper_2601_19362_b200 import partition as P
+
+    raw = P.generate_synthetic(("lognormal", 8.0, 1.5), 2048, 32768, 0)
+    return [max(512, x) for x in raw]
+
+
+def rank_plan(world, minibs, shape):
+    """LB-Mini plan (src/partition.cpp:490-580) -> per step, per rank: list of
+    microbatches (sample id lists)."""
+    from paper_2601_19362_b200 import partition as P
+
+    lens = workload_lengths()
+    steps = P.plan_flat("lb-mini", lens, world, minibs, 32768, P.CostModel(1.0, shape.beta_over_alpha(), 1))
+    return lens, steps
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][2]) if self.rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_sample(world, elems, micro):
+    """Times the reference's CPU fabric (ShardFabric<float>) on a bounded
+    sample: one FSDP unit, `world` simulated ranks, each client fetching twice
+    and pushing once (one microbatch of one unit), then finalize. Returns
+    (seconds, bytes_equiv, kind, sample)."""
+    from oracle import refbind as R
+
+    gathers, pushes = 2, 1
+    # same logical work, normalised to the B200 path's dtypes (bf16 fetch, fp32 push)
+    bytes_equiv = world * (gathers * elems * P2_BYTES_BF16 + pushes * elems * P4_BYTES_F32)
+    if R.available():
+        sec = R.fabric_seconds_f32(world, elems, gathers, pushes, 1)
+        return sec, bytes_equiv, "reference", (f"ShardFabric<float>({world}, {elems}) from oracle/_ref: "
+                                                f"{world} clients x ({gathers} gather + {pushes} scatter_accumulate)"
+                                                f" + finalize_minibatch, one FSDP unit of one microbatch")
+    import numpy as np
+
+    from oracle import odc_oracle as O
+
+    f = O.ShardFabric(world, elems, np.float32)
+    f.set_params("u", np.zeros(elems, np.float32))
+    g = np.ones(elems, np.float32)
+    t = time.perf_counter()
+    for c in range(world):
+        for _ in range(gathers):
+            f.gather(c, "u")
+        f.scatter_accumulate(c, g, np.float32(1.0 / world))
+    f.finalize_minibatch()
+    return time.perf_counter() - t, bytes_equiv, "port", "oracle port (numpy), same sample"
+
+
+def run_reference(args):
+    from paper_2601_19362_b200.shapes import SHAPES
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    shape = SHAPES[args.model]
+    world = args.gpus
+    for _ in range(args.warmup):
+        cpu_reference_sample(world, shape.layer_elems, 1)
+    secs, byts = 0.0, 0
+    for _ in range(args.steps):
+        s, b, kind, sample = cpu_reference_sample(world, shape.layer_elems, 1)
+        secs += s
+        byts += b
+    gbs = byts / secs / 1e9
+    line = {"metric": METRIC, "impl": "reference", "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": args.workload, "model": shape.name, "world": world},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": kind, "sample": sample},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_19362_b200 import _lib
+    from paper_2601_19362_b200.engine import OdcEngine
+    from paper_2601_19362_b200.shapes import SHAPES
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    shape = SHAPES[args.model]
+    L, M = shape.layers, shape.layer_elems
+    lens, steps = rank_plan(world, args.minibs, shape)
+
+    eng = OdcEngine([M] * L, rank=rank, world=world, device=local, push_mode=args.push_mode,
+                    fetch_ctas=args.fetch_ctas, push_ctas=args.push_ctas)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    init = torch.empty(M, device=dev)
+    for l in range(L):
+        init.normal_(0, 0.02, generator=g)
+        eng.set_params(l, init)
+    del init
+    bufs = [torch.empty(M, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    grad = torch.empty(M, dtype=torch.float32, device=dev).normal_(0, 1e-3, generator=g)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    kern = {"fetch": [], "push": []}  # (start, end) event pairs on the launching stream
+
+    def one_step(k, timed=False, host=None):
+        plan = steps[k % len(steps)][rank]
+        tok = [sum(lens[i] for i in mb) for mb in plan]
+        total = float(sum(sum(lens[i] for i in mb) for dv in steps[k % len(steps)] for mb in dv))
+        for t in tok:
+            w = t / total
+            for l in range(L):  # forward: fetch every unit
+                if timed:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                eng.fetch(l, bufs[l % 2])
+                if timed:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(stream)
+                    kern["fetch"].append((e0, e1))
+                if host is not None:
+                    host["fetch"].copy_(bufs[l % 2], non_blocking=True)
+            for l in reversed(range(L)):  # backward: re-fetch + push
+                eng.fetch(l, bufs[l % 2])
+                if host is not None:
+                    host["fetch"].copy_(bufs[l % 2], non_blocking=True)
+                    grad.copy_(host["grad"], non_blocking=True)
+                if timed:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                eng.push(l, grad, w)
+                if timed:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(stream)
+                    kern["push"].append((e0, e1))
+        eng.minibatch_end()
+        eng.adam_step(lr=1e-5, weight_decay=0.0)
+        return len(tok)
+
+    def timed_region(K, host=None, record=False):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        n_before = _lib.kernel_launches()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        micro = 0
+        for k in range(K):
+            micro += one_step(k, timed=record, host=host)
+        b.record(stream)
+        torch.cuda.synchronize()
+        eng.check()
+        ms = a.elapsed_time(b)
+        launches = _lib.kernel_launches() - n_before
+        if world > 1:
+            dist.barrier()
+        return ms, micro, launches
+
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    eng.check()
+
+    with ClockSampler(local) as clk:
+        ms, micro, launches = timed_region(args.steps, record=True)
+    bytes_rank = micro * L * M * (2 * P2_BYTES_BF16 + P4_BYTES_F32)
+    t = torch.tensor([ms, float(bytes_rank), float(micro), float(launches)], device=dev, dtype=torch.float64)
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, bytes_all, micro_all, launches_all = mx[0].item(), sm[1].item(), sm[2].item(), sm[3].item()
+    else:
+        ms_max, bytes_all, micro_all, launches_all = ms, float(bytes_rank), float(micro), float(launches)
+    value = bytes_all / (ms_max / 1e3) / 1e9
+    tokens_step = sum(lens[i] for s in range(args.steps) for dv in steps[s % len(steps)] for mb in dv for i in mb)
+
+    # per-kernel durations measured live in the timed region
+    def avg_ms(pairs):
+        return sum(e0.elapsed_time(e1) for e0, e1 in pairs) / max(1, len(pairs))
+
+    f_ms, p_ms = avg_ms(kern["fetch"]), avg_ms(kern["push"])
+    hbm, hbm_kind = peaks()
+    if world == 1:
+        # local HBM copy: read + write of the whole unit
+        f_bytes = M * P2_BYTES_BF16 * 2
+        roof = {"bound": "hbm", "achieved": round(f_bytes / (f_ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                "peak_kind": hbm_kind, "kernel": "copy_segments_kernel (odc_fetch)", "ms_per_launch": round(f_ms, 4),
+                "bytes_per_launch": f_bytes, "traffic": None}
+    else:
+        f_bytes = (world - 1) * ((M + world - 1) // world) * P2_BYTES_BF16  # NVLink ingress per launch
+        roof = {"bound": "nvlink", "achieved": round(f_bytes / (f_ms / 1e3) / 1e9, 1), "peak": NVLINK_NOMINAL_GBS,
+                "unit": "GB/s", "peak_kind": "nominal per-direction", "kernel": "copy_segments_kernel (odc_fetch)",
+                "ms_per_launch": round(f_ms, 4), "bytes_per_launch": f_bytes, "traffic": None}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    # N=1: read g + read-modify-write of the local fp32 shard (12 B/elem); N>1: NVLink egress
+    push_bytes = M * 12 if world == 1 else (world - 1) * ((M + world - 1) // world) * P4_BYTES_F32
+    push_info = {"kernel": "push_red_kernel" if args.push_mode == "red" else "slot_accumulate_kernel",
+                 "ms_per_launch": round(p_ms, 4), "GBps": round(push_bytes / (p_ms / 1e3) / 1e9, 1)}
+
+    # e2e through host buffers (reference-facing by-value I/O)
+    e2e = None
+    if not args.no_e2e:
+        host = {"fetch": torch.empty(M, dtype=torch.bfloat16, pin_memory=True),
+                "grad": torch.empty(M, dtype=torch.float32, pin_memory=True).normal_(0, 1e-3)}
+        K2 = 1
+        ms2, micro2, _ = timed_region(K2, host=host)
+        t2 = torch.tensor([ms2, float(micro2 * L * M * (2 * P2_BYTES_BF16 + P4_BYTES_F32))], device=dev,
+                          dtype=torch.float64)
+        if world > 1:
+            mx2 = t2.clone()
+            dist.all_reduce(mx2, op=dist.ReduceOp.MAX)
+            sm2 = t2.clone()
+            dist.all_reduce(sm2, op=dist.ReduceOp.SUM)
+            ms2, b2 = mx2[0].item(), sm2[1].item()
+        else:
+            b2 = t2[1].item()
+        e2e = {"value": round(b2 / (ms2 / 1e3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(micro2 * L * M * P4_BYTES_F32 / K2),
+               "d2h_bytes_per_step": int(micro2 * L * M * 2 * P2_BYTES_BF16 / K2),
+               "note": "fetched units copied to pinned host, pushed grads from pinned host (by-value API)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, b, kind, sample = cpu_reference_sample(1, M, 1)
+        cpu = {"value": round(b / s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": args.workload, "model": shape.name, "units": L, "unit_elems": M,
+                           "plan": "lb-mini", "minibs_per_rank": args.minibs, "budget_tokens": 32768,
+                           "lengths": "lognormal(8,1.5) n=2048 cap=32768 seed=0, floor 512",
+                           "push_mode": args.push_mode, "parallelism": f"odc{world}",
+                           "l2": "inputs > L2 (5.2 GB of units per pass), no flush",
+                           "microbatches_all_ranks": int(micro_all), "tokens_in_timed_steps": tokens_step},
+                "roofline": roof, "push": push_info, "clocks": clk.summary(), "e2e": e2e,
+                "cpu_baseline": cpu, "gpu_launches": int(launches_all)}
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+/*
+ * odc.h — C ABI of the B200-native On-Demand Communication (ODC) hot path.
+ *
+ * Two object kinds share the same sm_100a kernels:
+ *
+ *  odc_fabric_t  The reference's ShardFabric<T>/ShardState<T> (one FSDP unit,
+ *                all simulated ranks in this process, shards resident in HBM
+ *                on one device). Host-buffer I/O, synchronous, exactly the
+ *                reference's by-value semantics. Backs the drop-in C++ façade
+ *                include/odcsim/primitives.hpp.
+ *                  replaces inc/primitives.hpp:35-207 (ShardState, ShardFabric)
+ *
+ *  odc_ctx_t     The production engine: one rank per process (or host thread)
+ *                per GPU, every FSDP unit (layer) of a model, owner shards in
+ *                one HBM arena exported to peers with CUDA IPC handles.
+ *                Device pointers, stream-ordered, asynchronous; cross-rank
+ *                synchronisation is device-side only (sys-scope flags).
+ *
+ * Status codes map 1:1 onto the reference exception taxonomy
+ * (inc/types.hpp:14-48); the façade rethrows them. No C++ exception ever
+ * crosses this boundary. odc_last_error() returns a thread-local message.
+ *
+ * Reference paths: inc/ = /root/reference/proj/include/odcsim/,
+ *                  src/ = /root/reference/proj/src/.
+ */
+#ifndef ODC_ODC_H
+#define ODC_ODC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ODC_ABI_VERSION 1
+
+typedef enum {
+    ODC_OK = 0,
+    ODC_ERR_PARAM = 2,      /* ParamError / FormatError      inc/types.hpp:14-21 */
+    ODC_ERR_INFEASIBLE = 3, /* InfeasibleError                inc/types.hpp:23-27 */
+    ODC_ERR_INVARIANT = 4,  /* InvariantError                 inc/types.hpp:45-48 */
+    ODC_ERR_PROTOCOL = 5,   /* ProtocolError                  inc/types.hpp:35-38 */
+    ODC_ERR_STATE = 6,      /* StateError                     inc/types.hpp:40-43 */
+    ODC_ERR_MODE = 7,       /* ModeError                      inc/types.hpp:29-33 */
+    ODC_ERR_CUDA = 8,       /* CUDA runtime failure (no reference counterpart) */
+    ODC_ERR_TIMEOUT = 9     /* device barrier watchdog fired (no reference counterpart) */
+} odc_status;
+
+typedef enum { ODC_I64 = 0, ODC_F64 = 1, ODC_F32 = 2, ODC_BF16 = 3 } odc_dtype;
+
+typedef enum {
+    /* remote red.global.add.v4.f32 straight into the owner's fp32 gradient
+     * shard over NVLink; order across clients is not fixed */
+    ODC_PUSH_RED = 0,
+    /* deterministic: per-source slot (single writer, push order), reduced by
+     * the owner at the minibatch barrier in fixed rank order 0..N-1 */
+    ODC_PUSH_SLOT = 1
+} odc_push_mode;
+
+int odc_abi_version(void);
+const char* odc_last_error(void);
+/* number of sm_100a kernel launches issued by this process so far */
+uint64_t odc_kernel_launches(void);
+
+/* ---------------------------------------------------------------------------
+ * (a1) block shard layout.  inc/primitives.hpp:38-56
+ *   block = ceil(elems / ranks); begin = min(elems, r*block);
+ *   len = min(elems, (r+1)*block) - begin   (trailing ranks may own 0)
+ * ------------------------------------------------------------------------- */
+odc_status odc_shard_range(int64_t elems, int ranks, int rank, int64_t* begin, int64_t* len);
+
+/* ---------------------------------------------------------------------------
+ * Fabric: ShardFabric<T> / ShardState<T>.   inc/primitives.hpp:35-207
+ * dtype in {ODC_I64, ODC_F64, ODC_F32}. `weight` points at one T.
+ * ------------------------------------------------------------------------- */
+typedef struct odc_fabric* odc_fabric_t;
+
+/* ShardState(ranks, elems) :38-48 — ParamError if ranks < 1 or elems < 1 */
+odc_status odc_fabric_create(int ranks, int64_t elems, odc_dtype dtype, int device, odc_fabric_t* out);
+odc_status odc_fabric_destroy(odc_fabric_t f);
+/* scatter_accumulate strategy: ODC_PUSH_SLOT (default) = the reference's
+ * staged protocol (stage into the (owner, client) slot, the owner consumes the
+ * previous occupant first) — bit-exact in every dtype; ODC_PUSH_RED = remote
+ * red.add straight into the owner shard (bit-exact for I64). */
+odc_status odc_fabric_set_push_mode(odc_fabric_t f, odc_push_mode mode);
+/* set_params :58-67 (ParamError on length mismatch); host_full has `elems` T */
+odc_status odc_fabric_set_params(odc_fabric_t f, const char* id, const void* host_full, int64_t n);
+/* gather :70-77 — fetch kernel concatenates the owners' shards; StateError if unset */
+odc_status odc_fabric_gather(odc_fabric_t f, int client, const char* id, void* host_out);
+/* scatter_accumulate :181-188 — ParamError on length mismatch */
+odc_status odc_fabric_scatter_accumulate(odc_fabric_t f, int client, const void* host_grad, int64_t n,
+                                         const void* weight);
+/* push_slice :191-195 — ProtocolError if n > block or the slice overruns the target shard */
+odc_status odc_fabric_push_slice(odc_fabric_t f, int client, int target, int64_t offset,
+                                 const void* host_payload, int64_t n, const void* weight);
+/* finalize_minibatch :199-203 — drains every slot in (server, client) order,
+ * writes the N shards concatenated (= elems T) and zeroes them */
+odc_status odc_fabric_finalize(odc_fabric_t f, void* host_out);
+
+/* ShardState protocol steps (drivers run_schedule / run_threaded :242-359) */
+odc_status odc_fabric_split_stage(odc_fabric_t f, int from, int target, int64_t offset,
+                                  const void* host_payload, int64_t n, const void* weight, int* staged);
+odc_status odc_fabric_slot_free(odc_fabric_t f, int server, int client, int* is_free);
+odc_status odc_fabric_consume(odc_fabric_t f, int server, int client, int* did);
+odc_status odc_fabric_any_staged(odc_fabric_t f, int server, int* any);
+odc_status odc_fabric_take_grads(odc_fabric_t f, void* host_out);
+odc_status odc_fabric_max_staged(odc_fabric_t f, int server, int64_t* peak);
+
+/* ---------------------------------------------------------------------------
+ * Engine (one rank per GPU).
+ * ------------------------------------------------------------------------- */
+typedef struct odc_ctx* odc_ctx_t;
+
+typedef struct {
+    int rank;
+    int world;
+    int device;
+    int n_layers;               /* FSDP units */
+    const int64_t* layer_elems; /* elements per unit, n_layers entries */
+    int push_mode;              /* odc_push_mode */
+    int fetch_ctas;             /* CTAs for fetch (0 = default): non-intrusive SM budget */
+    int push_ctas;              /* CTAs for push  (0 = default) */
+    double timeout_s;           /* device barrier watchdog (<= 0: 60 s) */
+} odc_config;
+
+odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out);
+odc_status odc_ctx_destroy(odc_ctx_t ctx);
+/* IPC blob describing this rank's HBM arena (cudaIpcMemHandle + layout hash) */
+odc_status odc_ctx_export(odc_ctx_t ctx, void* blob, size_t cap, size_t* len);
+odc_status odc_ctx_import(odc_ctx_t ctx, int peer, const void* blob, size_t len);
+/* after every peer was imported: builds the device pointer tables */
+odc_status odc_ctx_ready(odc_ctx_t ctx);
+/* bytes of HBM the arena holds on this rank */
+odc_status odc_ctx_arena_bytes(odc_ctx_t ctx, int64_t* bytes);
+
+/* set_params: copy this rank's owned slice [begin, begin+len) of the full
+ * fp32 unit `src_full` (device) into the owner's fp32 master + bf16 shard. */
+odc_status odc_set_params(odc_ctx_t ctx, int layer, const float* src_full, void* stream);
+/* (a3) fetch: dst_full (bf16, elems) = concat of all owners' bf16 shards;
+ * waits (device-side) for each owner's current parameter epoch. */
+odc_status odc_fetch(odc_ctx_t ctx, int layer, void* dst_full_bf16, void* stream);
+/* fetch variant returning fp32 masters (parity / debugging) */
+odc_status odc_fetch_master(odc_ctx_t ctx, int layer, float* dst_full, void* stream);
+/* (a6) push: owner_grad += weight * grad_full[owner range] for every owner.
+ * grad dtype ODC_F32 or ODC_BF16. */
+odc_status odc_push(odc_ctx_t ctx, int layer, const void* grad_full, int grad_dtype, float weight,
+                    void* stream);
+/* (a7) push_slice: ProtocolError if n > block or offset+n > shard_len(target) */
+odc_status odc_push_slice(odc_ctx_t ctx, int layer, int target, int64_t offset, const float* payload,
+                          int64_t n, float weight, void* stream);
+/* (a8) minibatch barrier: signal every owner, wait for every client, then
+ * (slot mode) reduce the per-source slots in rank order into the grad shard. */
+odc_status odc_minibatch_end(odc_ctx_t ctx, void* stream);
+/* read this rank's accumulated fp32 grad shard of `layer` (len = shard_len) */
+odc_status odc_read_grad_shard(odc_ctx_t ctx, int layer, float* dst, void* stream);
+odc_status odc_read_master_shard(odc_ctx_t ctx, int layer, float* dst, void* stream);
+
+typedef struct {
+    float lr, beta1, beta2, eps, weight_decay;
+    int step; /* 1-based, for bias correction */
+} odc_adam_cfg;
+/* (a19) fused AdamW over every owned shard (fp32 master/m/v, bf16 shard out),
+ * zeroes the grad shards, then publishes the new parameter epoch. In slot
+ * mode the rank-order slot reduce is fused into the same kernel. */
+odc_status odc_adam_step(odc_ctx_t ctx, const odc_adam_cfg* cfg, void* stream);
+/* host check of the device error word (watchdog); blocks on `stream` */
+odc_status odc_ctx_check(odc_ctx_t ctx, void* stream);
+/* current minibatch epoch (number of completed odc_minibatch_end calls) */
+int64_t odc_ctx_epoch(odc_ctx_t ctx);
+
+/* ---------------------------------------------------------------------------
+ * Raw kernels on caller-owned device memory (bench / FSDP comparison path).
+ * ------------------------------------------------------------------------- */
+/* multi-segment copy (16B vector path when src ≡ dst mod 16) */
+odc_status odc_copy_segments(int nseg, const void* const* srcs, void* const* dsts, const int64_t* bytes,
+                             int ctas, void* stream);
+/* L2 flush helper for timing hygiene: writes `bytes` of scratch */
+odc_status odc_l2_flush(void* scratch, int64_t bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Load balancer (host C++, bit-exact restatement).  src/partition.cpp
+ * strategy: 0 local-sort, 1 lb-micro, 2 lb-mini, 3 verl-native, 4 verl-optimized
+ * ------------------------------------------------------------------------- */
+/* plan() :490-580 serialised as solutions_to_json() (src/experiment.cpp:215-233),
+ * byte-identical to nlohmann::json::dump(). *needed = bytes incl. NUL. */
+odc_status odc_plan_json(int strategy, const int64_t* lens, int64_t n, int devices, int minibs,
+                         int64_t budget, double alpha, double beta, int layers, uint64_t seed, char* out,
+                         int64_t cap, int64_t* needed);
+/* flat plan: for each step s, device d, microbatch m: the sample ids.
+ * Layout (int64): [n_steps, then per step: n_dev, per dev: n_mb, per mb: n_ids, ids...]
+ * *needed = int64 words required. */
+odc_status odc_plan_flat(int strategy, const int64_t* lens, int64_t n, int devices, int minibs,
+                         int64_t budget, double alpha, double beta, uint64_t seed, int64_t* out, int64_t cap,
+                         int64_t* needed);
+/* kk_partition :84-128 as JSON {"parts":..,"sums":..,"spread":..} */
+odc_status odc_kk_partition_json(const double* costs, int n, int k, int equal_size, char* out, int64_t cap,
+                                 int64_t* needed);
+/* generate_synthetic + scale_lengths (src/workload.cpp:218-271);
+ * dist 0 lognormal(p1=mu,p2=sigma) 1 pareto(scale,shape) 2 uniform(lo,hi) */
+odc_status odc_generate_synthetic(int dist, double p1, double p2, int64_t n, int64_t cap, uint64_t seed,
+                                  double scale, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODC_ODC_H */

@@ -1,0 +1,573 @@
+// engine.cu — odc_ctx_t: the production ODC engine, one rank per GPU.
+//
+// HBM arena (one cudaMalloc per rank, exported once with cudaIpcGetMemHandle,
+// identical layout on every rank so peers can address each other's shards):
+//
+//   [flags page 4 KB]  done[r] u64 (written by client r at the barrier),
+//                      param_epoch u64 (owner publishes after AdamW), err u64
+//   per FSDP unit l, this rank's owned shard (block_l = ceil(M_l / N)):
+//     param  bf16 [block+8]  stored at pad = begin % 8   (co-aligned with the
+//     grad   f32  [block+4]  stored at pad = begin % 4    caller's full-layer
+//     master f32  [block+4]                               buffers, so fetch
+//     m, v   f32  [block+4]                               and push run the
+//     slot   f32  [M_l]      (SLOT push mode only)        16-byte vector path)
+//
+// Mapping onto the reference (inc/ = /root/reference/proj/include/odcsim/):
+//   layout          ShardState ctor/shard_begin/shard_len     inc/primitives.hpp:38-56
+//   odc_set_params  ShardState::set_params                    :58-67
+//   odc_fetch       ShardState::gather                        :70-77
+//   odc_push        ShardFabric::scatter_accumulate           :181-188
+//   odc_push_slice  ShardFabric::push_slice (ProtocolError)   :191-195, :105-112
+//   odc_minibatch_end + odc_read_grad_shard
+//                   ShardFabric::finalize_minibatch/take_grads :199-203, :144-148
+//   odc_adam_step   (no reference counterpart: the reference only accumulates)
+//
+// Ordering protocol (all device-side, sys scope):
+//   * fetch of owner r's shard waits param_epoch[r] >= adams completed here;
+//   * RED push into owner r waits the same gate (its grad shard was zeroed by
+//     that AdamW); SLOT push waits every owner (they finished reading slots);
+//   * minibatch_end: st.release.sys done[rank] into every owner, then waits
+//     ld.acquire.sys done[c] >= epoch for every client c;
+//   * AdamW then st.release.sys param_epoch = ++adams.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace odc {
+namespace {
+thread_local std::string t_last_error;
+}
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+}  // namespace odc
+
+namespace {
+
+using odcsim::ParamError;
+using odcsim::ProtocolError;
+using odcsim::StateError;
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr std::int64_t kFlagsBytes = 4096;
+constexpr std::int64_t kDoneOff = 0;
+constexpr std::int64_t kEpochOff = 1024;
+constexpr std::int64_t kErrOff = 2048;
+constexpr std::uint64_t kBlobMagic = 0x4f44433142323030ULL;  // "ODC1B200"
+
+std::int64_t round256(std::int64_t x) { return (x + 255) / 256 * 256; }
+
+struct Unit {
+    std::int64_t elems = 0, block = 0;
+    std::int64_t off_param = 0, off_grad = 0, off_master = 0, off_m = 0, off_v = 0, off_slot = -1;
+    std::int64_t begin(int r) const { return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r) * block); }
+    std::int64_t len(int r) const { return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r + 1) * block) - begin(r); }
+};
+
+struct Blob {
+    std::uint64_t magic;
+    std::int32_t rank, world;
+    std::int64_t arena_bytes;
+    std::uint64_t layout_hash;
+    cudaIpcMemHandle_t handle;
+};
+
+}  // namespace
+
+struct odc_ctx {
+    odc_config cfg{};
+    std::vector<Unit> units;
+    std::int64_t arena_bytes = 0;
+    std::uint64_t layout_hash = 0;
+    char* arena = nullptr;
+    std::vector<char*> peer;  // peer[r] = r's arena mapped here (peer[rank] = arena)
+    std::vector<bool> imported;
+    bool ready = false;
+    long long timeout_ns = 60LL * 1000 * 1000 * 1000;
+    std::uint64_t mb_epoch = 0;  // completed minibatch_end calls
+    std::uint64_t adams = 0;     // completed adam steps (published param epochs)
+    std::vector<char> pushed;    // SLOT: unit touched in the current minibatch
+    odc::AdamSeg* d_segs = nullptr;
+    std::int64_t* d_seg_start = nullptr;
+    std::int64_t adam_units = 0;
+
+    int world() const { return cfg.world; }
+    int rank() const { return cfg.rank; }
+    bool slot_mode() const { return cfg.push_mode == ODC_PUSH_SLOT; }
+
+    char* at(int r, std::int64_t off) const { return peer[static_cast<std::size_t>(r)] + off; }
+    unsigned long long* done_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kDoneOff)); }
+    unsigned long long* epoch_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kEpochOff)); }
+    unsigned long long* err() const { return reinterpret_cast<unsigned long long*>(arena + kErrOff); }
+    // element 0 of owner r's shard of unit u in each array
+    unsigned short* param_of(int r, const Unit& u) const {
+        return reinterpret_cast<unsigned short*>(at(r, u.off_param)) + u.begin(r) % 8;
+    }
+    float* f32_of(int r, std::int64_t off, const Unit& u) const {
+        return reinterpret_cast<float*>(at(r, off)) + u.begin(r) % 4;
+    }
+    const Unit& unit(int l) const {
+        if (l < 0 || l >= static_cast<int>(units.size())) throw ParamError("layer index out of range");
+        return units[static_cast<std::size_t>(l)];
+    }
+    void need_ready() const {
+        if (!ready) throw StateError("odc context used before odc_ctx_ready()");
+    }
+    void dev() const { cuda_ok(cudaSetDevice(cfg.device), "cudaSetDevice"); }
+    // rotation: rank r visits owners r+1, r+2, ..., r so that concurrent
+    // fetches/pushes from all ranks spread over all owners' links
+    int owner_at(int i) const { return (rank() + 1 + i) % world(); }
+};
+
+namespace {
+
+odc_ctx* C(odc_ctx_t c) {
+    if (!c) throw ParamError("null odc context");
+    return c;
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int odc_abi_version(void) { return ODC_ABI_VERSION; }
+const char* odc_last_error(void) { return odc::t_last_error.c_str(); }
+std::uint64_t odc_kernel_launches(void) { return odc::launches(); }
+
+odc_status odc_shard_range(std::int64_t elems, int ranks, int rank, std::int64_t* begin, std::int64_t* len) {
+    return odc::guard([&] {
+        if (ranks < 1 || elems < 1) throw ParamError("need ranks >= 1 and elems >= 1");
+        if (rank < 0 || rank >= ranks) throw ParamError("rank out of range");
+        const std::int64_t block = (elems + ranks - 1) / ranks;
+        const std::int64_t b = std::min<std::int64_t>(elems, static_cast<std::int64_t>(rank) * block);
+        *begin = b;
+        *len = std::min<std::int64_t>(elems, static_cast<std::int64_t>(rank + 1) * block) - b;
+    });
+}
+
+odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
+    return odc::guard([&] {
+        if (!cfg || !out) throw ParamError("null config");
+        if (cfg->world < 1 || cfg->world > odc::kMaxSeg) throw ParamError("world must be 1..16");
+        if (cfg->rank < 0 || cfg->rank >= cfg->world) throw ParamError("rank out of range");
+        if (cfg->n_layers < 1 || !cfg->layer_elems) throw ParamError("need at least one FSDP unit");
+        if (cfg->push_mode != ODC_PUSH_RED && cfg->push_mode != ODC_PUSH_SLOT) throw ParamError("bad push mode");
+        auto* c = new odc_ctx();
+        try {
+            c->cfg = *cfg;
+            c->cfg.layer_elems = nullptr;
+            if (cfg->timeout_s > 0) c->timeout_ns = static_cast<long long>(cfg->timeout_s * 1e9);
+            std::int64_t off = kFlagsBytes;
+            std::uint64_t h = 1469598103934665603ULL;
+            auto mix = [&](std::uint64_t v) { h = (h ^ v) * 1099511628211ULL; };
+            mix(static_cast<std::uint64_t>(cfg->world));
+            mix(static_cast<std::uint64_t>(cfg->push_mode));
+            for (int l = 0; l < cfg->n_layers; ++l) {
+                Unit u;
+                u.elems = cfg->layer_elems[l];
+                if (u.elems < 1) throw ParamError("every FSDP unit needs elems >= 1");
+                u.block = (u.elems + cfg->world - 1) / cfg->world;
+                mix(static_cast<std::uint64_t>(u.elems));
+                u.off_param = off;
+                off += round256((u.block + 8) * 2);
+                const std::int64_t f32 = round256((u.block + 4) * 4);
+                u.off_grad = off;
+                off += f32;
+                u.off_master = off;
+                off += f32;
+                u.off_m = off;
+                off += f32;
+                u.off_v = off;
+                off += f32;
+                if (cfg->push_mode == ODC_PUSH_SLOT) {
+                    u.off_slot = off;
+                    off += round256(u.elems * 4);
+                }
+                c->units.push_back(u);
+            }
+            c->arena_bytes = off;
+            c->layout_hash = h;
+            c->dev();
+            cuda_ok(cudaMalloc(&c->arena, static_cast<std::size_t>(off)), "cudaMalloc arena");
+            cuda_ok(cudaMemset(c->arena, 0, static_cast<std::size_t>(off)), "memset arena");
+            c->peer.assign(static_cast<std::size_t>(cfg->world), nullptr);
+            c->imported.assign(static_cast<std::size_t>(cfg->world), false);
+            c->peer[static_cast<std::size_t>(cfg->rank)] = c->arena;
+            c->imported[static_cast<std::size_t>(cfg->rank)] = true;
+            c->pushed.assign(c->units.size(), 0);
+        } catch (...) {
+            odc_ctx_destroy(c);
+            throw;
+        }
+        *out = c;
+    });
+}
+
+odc_status odc_ctx_destroy(odc_ctx_t c) {
+    if (!c) return ODC_OK;
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    for (int r = 0; r < static_cast<int>(c->peer.size()); ++r)
+        if (r != c->cfg.rank && c->peer[static_cast<std::size_t>(r)]) cudaIpcCloseMemHandle(c->peer[static_cast<std::size_t>(r)]);
+    if (c->arena) cudaFree(c->arena);
+    if (c->d_segs) cudaFree(c->d_segs);
+    if (c->d_seg_start) cudaFree(c->d_seg_start);
+    delete c;
+    return ODC_OK;
+}
+
+odc_status odc_ctx_export(odc_ctx_t ch, void* blob, std::size_t cap, std::size_t* len) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        if (len) *len = sizeof(Blob);
+        if (!blob || cap < sizeof(Blob)) throw ParamError("export buffer too small");
+        c->dev();
+        Blob b{};
+        b.magic = kBlobMagic;
+        b.rank = c->rank();
+        b.world = c->world();
+        b.arena_bytes = c->arena_bytes;
+        b.layout_hash = c->layout_hash;
+        cuda_ok(cudaIpcGetMemHandle(&b.handle, c->arena), "cudaIpcGetMemHandle");
+        std::memcpy(blob, &b, sizeof b);
+    });
+}
+
+odc_status odc_ctx_import(odc_ctx_t ch, int peer, const void* blob, std::size_t len) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        if (peer < 0 || peer >= c->world()) throw ParamError("peer out of range");
+        if (peer == c->rank()) return;  // own arena is already mapped
+        if (!blob || len < sizeof(Blob)) throw ParamError("bad IPC blob");
+        Blob b;
+        std::memcpy(&b, blob, sizeof b);
+        if (b.magic != kBlobMagic || b.rank != peer || b.world != c->world())
+            throw ParamError("IPC blob does not belong to this peer/world");
+        if (b.layout_hash != c->layout_hash || b.arena_bytes != c->arena_bytes)
+            throw ParamError("peer arena layout differs (different layer sizes or push mode)");
+        c->dev();
+        void* p = nullptr;
+        cuda_ok(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        c->peer[static_cast<std::size_t>(peer)] = static_cast<char*>(p);
+        c->imported[static_cast<std::size_t>(peer)] = true;
+    });
+}
+
+odc_status odc_ctx_ready(odc_ctx_t ch) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        for (int r = 0; r < c->world(); ++r)
+            if (!c->imported[static_cast<std::size_t>(r)]) throw StateError("peer " + std::to_string(r) + " not imported");
+        c->dev();
+        // AdamW segment table over this rank's owned shards
+        std::vector<odc::AdamSeg> segs;
+        std::vector<std::int64_t> start{0};
+        for (const Unit& u : c->units) {
+            const int r = c->rank();
+            odc::AdamSeg s{};
+            s.master = c->f32_of(r, u.off_master, u);
+            s.m = c->f32_of(r, u.off_m, u);
+            s.v = c->f32_of(r, u.off_v, u);
+            s.grad = c->f32_of(r, u.off_grad, u);
+            s.param = c->param_of(r, u);
+            s.n = u.len(r);
+            segs.push_back(s);
+            const std::int64_t h = u.begin(r) % 4;
+            start.push_back(start.back() + (s.n > 0 ? (h + s.n + 3) / 4 : 0));
+        }
+        cuda_ok(cudaMalloc(&c->d_segs, segs.size() * sizeof(odc::AdamSeg)), "malloc segs");
+        cuda_ok(cudaMalloc(&c->d_seg_start, start.size() * sizeof(std::int64_t)), "malloc seg_start");
+        cuda_ok(cudaMemcpy(c->d_segs, segs.data(), segs.size() * sizeof(odc::AdamSeg), cudaMemcpyHostToDevice), "H2D segs");
+        cuda_ok(cudaMemcpy(c->d_seg_start, start.data(), start.size() * 8, cudaMemcpyHostToDevice), "H2D start");
+        c->adam_units = start.back();
+        c->ready = true;
+    });
+}
+
+odc_status odc_ctx_arena_bytes(odc_ctx_t ch, std::int64_t* bytes) {
+    return odc::guard([&] { *bytes = C(ch)->arena_bytes; });
+}
+
+int64_t odc_ctx_epoch(odc_ctx_t ch) { return ch ? static_cast<int64_t>(ch->mb_epoch) : -1; }
+
+odc_status odc_set_params(odc_ctx_t ch, int layer, const float* src_full, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        c->dev();
+        const int r = c->rank();
+        cuda_ok(odc::launch_init_shard(c->f32_of(r, u.off_master, u), c->param_of(r, u), src_full + u.begin(r), u.len(r),
+                                       S(stream)),
+                "set_params");
+    });
+}
+
+odc_status odc_fetch(odc_ctx_t ch, int layer, void* dst_full, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        c->dev();
+        odc::SegTable t{};
+        t.n = c->world();
+        for (int i = 0; i < c->world(); ++i) {
+            const int r = c->owner_at(i);
+            t.src[i] = reinterpret_cast<const char*>(c->param_of(r, u));
+            t.dst[i] = static_cast<char*>(dst_full) + u.begin(r) * 2;
+            t.bytes[i] = u.len(r) * 2;
+            t.gate[i] = c->epoch_of(r);
+        }
+        t.need = c->adams;
+        t.err = c->err();
+        t.timeout_ns = c->timeout_ns;
+        cuda_ok(odc::launch_copy_segments(t, c->cfg.fetch_ctas, S(stream)), "fetch");
+    });
+}
+
+odc_status odc_fetch_master(odc_ctx_t ch, int layer, float* dst_full, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        c->dev();
+        odc::SegTable t{};
+        t.n = c->world();
+        for (int i = 0; i < c->world(); ++i) {
+            const int r = c->owner_at(i);
+            t.src[i] = reinterpret_cast<const char*>(c->f32_of(r, u.off_master, u));
+            t.dst[i] = reinterpret_cast<char*>(dst_full + u.begin(r));
+            t.bytes[i] = u.len(r) * 4;
+            t.gate[i] = c->epoch_of(r);
+        }
+        t.need = c->adams;
+        t.err = c->err();
+        t.timeout_ns = c->timeout_ns;
+        cuda_ok(odc::launch_copy_segments(t, c->cfg.fetch_ctas, S(stream)), "fetch_master");
+    });
+}
+
+odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dtype, float weight, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        if (grad_dtype != ODC_F32 && grad_dtype != ODC_BF16) throw ParamError("grad dtype must be ODC_F32 or ODC_BF16");
+        const bool bf16 = grad_dtype == ODC_BF16;
+        c->dev();
+        if (c->slot_mode()) {
+            const unsigned long long* gates[odc::kMaxSeg];
+            for (int r = 0; r < c->world(); ++r) gates[r] = c->epoch_of(r);
+            const bool first = !c->pushed[static_cast<std::size_t>(layer)];
+            cuda_ok(odc::launch_slot_accumulate(reinterpret_cast<float*>(c->arena + u.off_slot), grad_full, bf16, u.elems,
+                                                weight, first, gates, first ? c->world() : 0, c->adams, c->err(),
+                                                c->timeout_ns, c->cfg.push_ctas, S(stream)),
+                    "slot push");
+            c->pushed[static_cast<std::size_t>(layer)] = 1;
+            return;
+        }
+        odc::RedTable t{};
+        t.n = c->world();
+        for (int i = 0; i < c->world(); ++i) {
+            const int r = c->owner_at(i);
+            t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
+            t.dst[i] = c->f32_of(r, u.off_grad, u);
+            t.elems[i] = u.len(r);
+            t.gate[i] = c->epoch_of(r);
+        }
+        t.need = c->adams;
+        t.err = c->err();
+        t.timeout_ns = c->timeout_ns;
+        cuda_ok(odc::launch_push_red(t, weight, bf16, c->cfg.push_ctas, S(stream)), "push");
+    });
+}
+
+odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offset, const float* payload,
+                          std::int64_t n, float weight, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        if (target < 0 || target >= c->world()) throw ParamError("target rank out of range");
+        if (n < 0) throw ParamError("negative payload length");
+        if (n > u.block)
+            throw ProtocolError("payload of " + std::to_string(n) + " elements exceeds the per-client buffer slot of " +
+                                std::to_string(u.block));
+        if (offset < 0 || offset + n > u.len(target)) throw ProtocolError("payload does not fit the target shard");
+        if (n == 0) return;
+        c->dev();
+        if (c->slot_mode()) {
+            float* slot = reinterpret_cast<float*>(c->arena + u.off_slot);
+            if (!c->pushed[static_cast<std::size_t>(layer)]) {
+                const unsigned long long* gates[odc::kMaxSeg];
+                for (int r = 0; r < c->world(); ++r) gates[r] = c->epoch_of(r);
+                float* p = slot;
+                std::int64_t cnt = u.elems;
+                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, gates, c->world(), c->adams, c->err(), c->timeout_ns,
+                                               S(stream)),
+                        "slot zero");
+                c->pushed[static_cast<std::size_t>(layer)] = 1;
+            }
+            cuda_ok(odc::launch_accumulate<float>(slot + u.begin(target) + offset, payload, n, weight, S(stream)),
+                    "slot slice");
+            return;
+        }
+        odc::RedTable t{};
+        t.n = 1;
+        t.src[0] = payload;
+        t.dst[0] = c->f32_of(target, u.off_grad, u) + offset;
+        t.elems[0] = n;
+        t.gate[0] = c->epoch_of(target);
+        t.need = c->adams;
+        t.err = c->err();
+        t.timeout_ns = c->timeout_ns;
+        cuda_ok(odc::launch_push_red(t, weight, false, 8, S(stream)), "push_slice");
+    });
+}
+
+odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        c->dev();
+        const unsigned long long* gates[odc::kMaxSeg];
+        for (int r = 0; r < c->world(); ++r) gates[r] = c->epoch_of(r);
+        if (c->slot_mode()) {
+            // units this rank never pushed this minibatch still hold last
+            // minibatch's sums: zero them once every owner finished reading
+            std::vector<float*> ptrs;
+            std::vector<std::int64_t> cnt;
+            for (std::size_t l = 0; l < c->units.size(); ++l)
+                if (!c->pushed[l]) {
+                    ptrs.push_back(reinterpret_cast<float*>(c->arena + c->units[l].off_slot));
+                    cnt.push_back(c->units[l].elems);
+                }
+            if (!ptrs.empty())
+                cuda_ok(odc::launch_gated_zero(ptrs.data(), cnt.data(), static_cast<int>(ptrs.size()), gates, c->world(),
+                                               c->adams, c->err(), c->timeout_ns, S(stream)),
+                        "slot zero");
+        }
+        odc::BarrierArgs a{};
+        a.world = c->world();
+        a.rank = c->rank();
+        for (int r = 0; r < c->world(); ++r) a.peer_done[r] = c->done_of(r);
+        a.my_done = c->done_of(c->rank());
+        a.epoch = c->mb_epoch + 1;
+        a.err = c->err();
+        a.timeout_ns = c->timeout_ns;
+        cuda_ok(odc::launch_barrier(a, S(stream)), "barrier");
+        c->mb_epoch += 1;
+        if (c->slot_mode()) {
+            const int me = c->rank();
+            for (const Unit& u : c->units) {
+                const float* srcs[odc::kMaxSeg];
+                for (int s = 0; s < c->world(); ++s)  // fixed rank order 0..N-1
+                    srcs[s] = reinterpret_cast<const float*>(c->at(s, u.off_slot)) + u.begin(me);
+                cuda_ok(odc::launch_reduce_sources(c->f32_of(me, u.off_grad, u), srcs, c->world(), u.len(me),
+                                                   c->cfg.push_ctas > 0 ? c->cfg.push_ctas : 0, S(stream)),
+                        "slot reduce");
+            }
+            std::fill(c->pushed.begin(), c->pushed.end(), 0);
+        }
+    });
+}
+
+odc_status odc_read_grad_shard(odc_ctx_t ch, int layer, float* dst, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        c->dev();
+        const int r = c->rank();
+        if (u.len(r) > 0)
+            cuda_ok(cudaMemcpyAsync(dst, c->f32_of(r, u.off_grad, u), static_cast<std::size_t>(u.len(r)) * 4,
+                                    cudaMemcpyDeviceToDevice, S(stream)),
+                    "read grad");
+    });
+}
+
+odc_status odc_read_master_shard(odc_ctx_t ch, int layer, float* dst, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        const Unit& u = c->unit(layer);
+        c->dev();
+        const int r = c->rank();
+        if (u.len(r) > 0)
+            cuda_ok(cudaMemcpyAsync(dst, c->f32_of(r, u.off_master, u), static_cast<std::size_t>(u.len(r)) * 4,
+                                    cudaMemcpyDeviceToDevice, S(stream)),
+                    "read master");
+    });
+}
+
+odc_status odc_adam_step(odc_ctx_t ch, const odc_adam_cfg* cfg, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->need_ready();
+        if (!cfg || cfg->step < 1) throw ParamError("adam step must be >= 1");
+        c->dev();
+        odc::AdamArgs a{};
+        a.segs = c->d_segs;
+        a.nseg = static_cast<int>(c->units.size());
+        a.seg_start = c->d_seg_start;
+        a.lr = cfg->lr;
+        a.beta1 = cfg->beta1;
+        a.beta2 = cfg->beta2;
+        a.eps = cfg->eps;
+        a.wd = cfg->weight_decay;
+        const double bc1 = 1.0 - std::pow(static_cast<double>(cfg->beta1), cfg->step);
+        const double bc2 = 1.0 - std::pow(static_cast<double>(cfg->beta2), cfg->step);
+        a.step_size = static_cast<float>(cfg->lr / bc1);
+        a.bc2_sqrt_inv = static_cast<float>(1.0 / std::sqrt(bc2));
+        cuda_ok(odc::launch_adam(a, c->adam_units, 0, S(stream)), "adam");
+        c->adams += 1;
+        cuda_ok(odc::launch_publish(c->epoch_of(c->rank()), c->adams, S(stream)), "publish epoch");
+    });
+}
+
+odc_status odc_ctx_check(odc_ctx_t ch, void* stream) {
+    unsigned long long e = 0;
+    odc_status st = odc::guard([&] {
+        odc_ctx* c = C(ch);
+        c->dev();
+        cuda_ok(cudaStreamSynchronize(S(stream)), "sync");
+        cuda_ok(cudaMemcpy(&e, c->err(), 8, cudaMemcpyDeviceToHost), "read err");
+    });
+    if (st != ODC_OK) return st;
+    if (e == odc::kErrTimeout) {
+        odc::set_last_error("device barrier watchdog fired: a peer never reached the minibatch barrier "
+                            "or never published its parameter epoch");
+        return ODC_ERR_TIMEOUT;
+    }
+    return ODC_OK;
+}
+
+odc_status odc_copy_segments(int nseg, const void* const* srcs, void* const* dsts, const std::int64_t* bytes, int ctas,
+                             void* stream) {
+    return odc::guard([&] {
+        if (nseg < 0 || nseg > odc::kMaxSeg) throw ParamError("1..16 segments per call");
+        odc::SegTable t{};
+        t.n = nseg;
+        for (int i = 0; i < nseg; ++i) {
+            t.src[i] = static_cast<const char*>(srcs[i]);
+            t.dst[i] = static_cast<char*>(dsts[i]);
+            t.bytes[i] = bytes[i];
+        }
+        cuda_ok(odc::launch_copy_segments(t, ctas, S(stream)), "copy_segments");
+    });
+}
+
+odc_status odc_l2_flush(void* scratch, std::int64_t bytes, void* stream) {
+    return odc::guard([&] { cuda_ok(odc::launch_l2_flush(scratch, bytes, S(stream)), "l2 flush"); });
+}
+
+}  // extern "C"

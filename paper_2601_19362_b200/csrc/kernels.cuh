@@ -1,0 +1,107 @@
+// kernels.cuh — launch interface of the ODC sm_100a kernels (odc_kernels.cu).
+// Every launcher is stream-ordered and bumps the process launch counter.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace odc {
+
+constexpr int kMaxSeg = 16;  // max ranks on one NVSwitch box we size tables for
+
+// Byte segments (fetch / set_params / read-back). src ≡ dst (mod 16) takes
+// the 16-byte vector path; any other pair falls back to 4/2/1-byte moves.
+struct SegTable {
+    int n = 0;
+    const char* src[kMaxSeg];
+    char* dst[kMaxSeg];
+    std::int64_t bytes[kMaxSeg];
+    // optional per-segment readiness gate: wait until *gate[i] >= need (sys scope)
+    const unsigned long long* gate[kMaxSeg];
+    unsigned long long need = 0;
+    unsigned long long* err = nullptr;  // device error word (watchdog)
+    long long timeout_ns = 0;
+};
+
+// fp32 reduction segments for push: dst[i] += w * src[i]
+struct RedTable {
+    int n = 0;
+    const void* src[kMaxSeg];  // grad slice (fp32 or bf16)
+    float* dst[kMaxSeg];       // owner's fp32 grad shard (peer memory)
+    std::int64_t elems[kMaxSeg];
+    const unsigned long long* gate[kMaxSeg];
+    unsigned long long need = 0;
+    unsigned long long* err = nullptr;
+    long long timeout_ns = 0;
+};
+
+enum : unsigned long long { kErrNone = 0, kErrTimeout = 1 };
+
+std::uint64_t launches();
+void count_launch();
+
+cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s);
+// push, RED mode: remote red.relaxed.sys.global.add(.v4).f32 into owner shards
+cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas, cudaStream_t s);
+// push, SLOT mode (deterministic, local): acc[i] = (assign ? 0 : acc[i]) + w*g[i]
+// after every owner in `gates` reached `need` (previous reduce finished)
+cudaError_t launch_slot_accumulate(float* acc, const void* grad, bool src_bf16, std::int64_t n, float w, bool assign,
+                                   const unsigned long long* const* gates, int ngates, unsigned long long need,
+                                   unsigned long long* err, long long timeout_ns, int ctas, cudaStream_t s);
+// owner reduce in fixed source order: dst[i] = sum_{c=0..nsrc-1} src[c][i]
+cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc, std::int64_t n, int ctas,
+                                  cudaStream_t s);
+
+// ---- the generic typed kernels behind the reference-semantics fabric ----
+// dst[i] = dst[i] + w * src[i]   (one multiply, one add, each rounded; no FMA)
+template <typename T>
+cudaError_t launch_accumulate(T* dst, const T* src, std::int64_t n, T w, cudaStream_t s);
+// dst[i] atomically += w * src[i]  (red.global.add: u64 / f64 / f32)
+template <typename T>
+cudaError_t launch_red_accumulate(T* dst, const T* src, std::int64_t n, T w, cudaStream_t s);
+
+// ---- barrier / flags ----
+// thread t < world: st.release.sys peer_done[t][my_slot] = epoch;
+// then thread t < world spins ld.acquire.sys my_done[t] >= epoch.
+struct BarrierArgs {
+    int world = 1;
+    int rank = 0;
+    unsigned long long* peer_done[kMaxSeg];  // owner t's done array base
+    const unsigned long long* my_done = nullptr;
+    unsigned long long epoch = 0;
+    unsigned long long* err = nullptr;
+    long long timeout_ns = 0;
+};
+cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
+// st.release.sys *flag = value (after everything earlier on the stream)
+cudaError_t launch_publish(unsigned long long* flag, unsigned long long value, cudaStream_t s);
+// wait for every gate >= need, then zero `n` floats at each of `ptrs`
+cudaError_t launch_gated_zero(float* const* ptrs, const std::int64_t* n, int count,
+                              const unsigned long long* const* gates, int ngates, unsigned long long need,
+                              unsigned long long* err, long long timeout_ns, cudaStream_t s);
+
+// ---- fused AdamW over owned shards ----
+struct AdamSeg {
+    float* master;
+    float* m;
+    float* v;
+    float* grad;              // fp32 grad shard (zeroed after use)
+    unsigned short* param;    // bf16 shard out
+    std::int64_t n;
+};
+struct AdamArgs {
+    const AdamSeg* segs = nullptr;  // device array
+    int nseg = 0;
+    const std::int64_t* seg_start = nullptr;  // device prefix of 4-element vector counts (nseg+1)
+    float lr, beta1, beta2, eps, wd;
+    float step_size;     // lr / (1 - beta1^t)
+    float bc2_sqrt_inv;  // 1 / sqrt(1 - beta2^t)
+};
+cudaError_t launch_adam(const AdamArgs& a, std::int64_t total_vec_units, int ctas, cudaStream_t s);
+
+cudaError_t launch_l2_flush(void* scratch, std::int64_t bytes, cudaStream_t s);
+// owner init: master[i] = src[i]; param[i] = bf16_rn(src[i])
+cudaError_t launch_init_shard(float* master, unsigned short* param, const float* src, std::int64_t n, cudaStream_t s);
+
+}  // namespace odc

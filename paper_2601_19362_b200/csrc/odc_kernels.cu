@@ -1,0 +1,645 @@
+// odc_kernels.cu — sm_100a kernels of the ODC hot path.
+//
+//   copy_segments   fetch (a3): N owner shards (peer HBM over NVLink + local)
+//                   -> one full-layer buffer. 16-byte vector loads, UNROLL
+//                   independent loads in flight per thread, chunked over a
+//                   small CTA budget so fetch stays non-intrusive.
+//                   replaces ShardState::gather inc/primitives.hpp:70-77
+//   push_red        push (a6), RED mode: red.relaxed.sys.global.add.v4.f32
+//                   straight into each owner's fp32 grad shard (NVLink).
+//                   replaces split_gradient + try_stage + consume :80-136
+//   slot_accumulate push (a6), SLOT mode: single-writer per-source slot
+//                   acc += w*g (local HBM), deterministic.
+//   reduce_sources  owner reduce in fixed rank order (SLOT mode barrier step)
+//   barrier         (a8) finalize_minibatch :199-203 as sys-scope flags
+//   adam            (a19) fused AdamW over owned shards, bf16 shard out
+//   accumulate<T>   ShardState::consume :125-136 exactly (mul, then add)
+//   red_accumulate<T> red.add.{u64,f64,f32} form of consume
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace odc {
+
+namespace {
+std::atomic<std::uint64_t> g_launches{0};
+}
+std::uint64_t launches() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+__host__ __device__ __forceinline__ std::int64_t i64min(std::int64_t a, std::int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ std::int64_t i64max(std::int64_t a, std::int64_t b) { return a > b ? a : b; }
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void red_sys_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void red_sys_f32(float* p, float a) {
+    asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ long long global_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Bounded spin: returns false (and raises the error word) on timeout so a
+// dead peer turns into ODC_ERR_TIMEOUT on the host instead of a hung GPU.
+__device__ bool wait_geq(const unsigned long long* flag, unsigned long long need, unsigned long long* err,
+                         long long timeout_ns) {
+    if (ld_acquire_sys(flag) >= need) return true;
+    const long long t0 = global_ns();
+    unsigned ns = 32;
+    while (true) {
+        if (ld_acquire_sys(flag) >= need) return true;
+        if (err && *reinterpret_cast<volatile unsigned long long*>(err) != kErrNone) return false;
+        if (global_ns() - t0 > timeout_ns) {
+            if (err) atomicExch(err, static_cast<unsigned long long>(kErrTimeout));
+            return false;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+    }
+}
+
+__device__ __forceinline__ float bf16_to_f32(unsigned short h) { return __uint_as_float(static_cast<unsigned>(h) << 16); }
+__device__ __forceinline__ unsigned short f32_to_bf16(float f) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// ------------------------------------------------------------ fetch / copy
+constexpr int kCopyThreads = 512;
+constexpr int kCopyUnroll = 8;
+constexpr std::int64_t kChunkVec = kCopyThreads * kCopyUnroll;  // 4096 x 16 B = 64 KB per chunk
+
+struct SegPlan {
+    std::int64_t head, vecs, tail;  // bytes before the aligned body, 16B units, bytes after
+    std::int64_t chunks;
+    bool fast;
+};
+
+__device__ __forceinline__ SegPlan plan_seg(const char* src, const char* dst, std::int64_t bytes) {
+    SegPlan p{};
+    if (bytes <= 0) return p;
+    const unsigned sa = static_cast<unsigned>(reinterpret_cast<uintptr_t>(src) & 15);
+    const unsigned da = static_cast<unsigned>(reinterpret_cast<uintptr_t>(dst) & 15);
+    p.fast = sa == da;
+    if (p.fast) {
+        p.head = i64min(bytes, (16 - da) & 15);
+        p.vecs = (bytes - p.head) / 16;
+        p.tail = bytes - p.head - p.vecs * 16;
+        p.chunks = i64max(1, (p.vecs + kChunkVec - 1) / kChunkVec);
+    } else {
+        p.chunks = (bytes + kChunkVec * 16 - 1) / (kChunkVec * 16);
+    }
+    return p;
+}
+
+__global__ void __launch_bounds__(kCopyThreads) copy_segments_kernel(SegTable t) {
+    __shared__ SegPlan plans[kMaxSeg];
+    __shared__ std::int64_t first_chunk[kMaxSeg + 1];
+    __shared__ int gate_ok;
+    if (threadIdx.x == 0) {
+        std::int64_t acc = 0;
+        for (int i = 0; i < t.n; ++i) {
+            plans[i] = plan_seg(t.src[i], t.dst[i], t.bytes[i]);
+            first_chunk[i] = acc;
+            acc += plans[i].chunks;
+        }
+        first_chunk[t.n] = acc;
+    }
+    __syncthreads();
+    const std::int64_t total = first_chunk[t.n];
+    int seg = 0;
+    int gated_seg = -1;
+    for (std::int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+        while (c >= first_chunk[seg + 1]) ++seg;
+        if (t.gate[seg] && gated_seg != seg) {  // on-demand readiness of this owner's shard
+            if (threadIdx.x == 0) gate_ok = wait_geq(t.gate[seg], t.need, t.err, t.timeout_ns);
+            __syncthreads();
+            const bool ok = gate_ok != 0;
+            __syncthreads();  // gate_ok may be rewritten at the next segment switch
+            gated_seg = seg;
+            if (!ok) continue;
+        }
+        const SegPlan p = plans[seg];
+        const char* src = t.src[seg];
+        char* dst = t.dst[seg];
+        const std::int64_t j = c - first_chunk[seg];
+        if (p.fast) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src + p.head);
+            uint4* d4 = reinterpret_cast<uint4*>(dst + p.head);
+            const std::int64_t beg = j * kChunkVec, end = i64min(p.vecs, beg + kChunkVec);
+            std::int64_t i = beg + threadIdx.x;
+            if (end - beg == kChunkVec) {
+                uint4 r[kCopyUnroll];
+#pragma unroll
+                for (int u = 0; u < kCopyUnroll; ++u) r[u] = ld_stream_v4(s4 + i + u * kCopyThreads);
+#pragma unroll
+                for (int u = 0; u < kCopyUnroll; ++u) st_v4(d4 + i + u * kCopyThreads, r[u]);
+            } else {
+                for (; i < end; i += kCopyThreads) st_v4(d4 + i, ld_stream_v4(s4 + i));
+            }
+            if (j == 0) {
+                if (threadIdx.x < p.head) dst[threadIdx.x] = src[threadIdx.x];
+                const std::int64_t tb = p.head + p.vecs * 16;
+                if (threadIdx.x < p.tail) dst[tb + threadIdx.x] = src[tb + threadIdx.x];
+            }
+        } else {
+            const std::int64_t beg = j * kChunkVec * 16, end = i64min(t.bytes[seg], beg + kChunkVec * 16);
+            for (std::int64_t b = beg + threadIdx.x; b < end; b += kCopyThreads) dst[b] = src[b];
+        }
+    }
+}
+
+cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s) {
+    if (t.n <= 0) return cudaSuccess;
+    if (ctas <= 0) ctas = 148;
+    count_launch();
+    copy_segments_kernel<<<ctas, kCopyThreads, 0, s>>>(t);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- push (RED)
+constexpr int kPushThreads = 512;
+constexpr int kPushUnroll = 4;
+constexpr std::int64_t kPushChunk = kPushThreads * kPushUnroll;  // 4-element units per chunk
+
+struct RedPlan {
+    std::int64_t head, units, tail, chunks;  // head/tail in elements, units of 4 elements
+    bool fast;
+};
+
+__device__ __forceinline__ RedPlan plan_red(const void* src, const float* dst, std::int64_t n, bool bf16) {
+    RedPlan p{};
+    if (n <= 0) return p;
+    const unsigned da = static_cast<unsigned>(reinterpret_cast<uintptr_t>(dst) & 15);  // multiple of 4
+    const std::int64_t head = i64min(n, ((16 - da) & 15) / 4);
+    const uintptr_t s_after = reinterpret_cast<uintptr_t>(src) + head * (bf16 ? 2 : 4);
+    p.fast = (da % 4 == 0) && (s_after % (bf16 ? 8 : 16) == 0);
+    if (p.fast) {
+        p.head = head;
+        p.units = (n - head) / 4;
+        p.tail = n - head - p.units * 4;
+        p.chunks = i64max(1, (p.units + kPushChunk - 1) / kPushChunk);
+    } else {
+        p.chunks = (n + kPushChunk * 4 - 1) / (kPushChunk * 4);
+    }
+    return p;
+}
+
+template <bool BF16>
+__device__ __forceinline__ float load_grad(const void* src, std::int64_t i) {
+    if constexpr (BF16) return bf16_to_f32(reinterpret_cast<const unsigned short*>(src)[i]);
+    else return reinterpret_cast<const float*>(src)[i];
+}
+
+template <bool BF16>
+__device__ __forceinline__ float4 load_grad4(const void* src, std::int64_t e) {
+    if constexpr (BF16) {
+        const uint2 v = *reinterpret_cast<const uint2*>(reinterpret_cast<const unsigned short*>(src) + e);
+        return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u), __uint_as_float(v.y << 16),
+                           __uint_as_float(v.y & 0xffff0000u));
+    } else {
+        return *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) + e);
+    }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kPushThreads) push_red_kernel(RedTable t, float w) {
+    __shared__ RedPlan plans[kMaxSeg];
+    __shared__ std::int64_t first_chunk[kMaxSeg + 1];
+    __shared__ int gate_ok;
+    if (threadIdx.x == 0) {
+        std::int64_t acc = 0;
+        for (int i = 0; i < t.n; ++i) {
+            plans[i] = plan_red(t.src[i], t.dst[i], t.elems[i], BF16);
+            first_chunk[i] = acc;
+            acc += plans[i].chunks;
+        }
+        first_chunk[t.n] = acc;
+    }
+    __syncthreads();
+    const std::int64_t total = first_chunk[t.n];
+    int seg = 0, gated_seg = -1;
+    for (std::int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+        while (c >= first_chunk[seg + 1]) ++seg;
+        if (t.gate[seg] && gated_seg != seg) {  // owner finished its previous Adam step
+            if (threadIdx.x == 0) gate_ok = wait_geq(t.gate[seg], t.need, t.err, t.timeout_ns);
+            __syncthreads();
+            const bool ok = gate_ok != 0;
+            __syncthreads();  // gate_ok may be rewritten at the next segment switch
+            gated_seg = seg;
+            if (!ok) continue;
+        }
+        const RedPlan p = plans[seg];
+        const void* src = t.src[seg];
+        float* dst = t.dst[seg];
+        const std::int64_t j = c - first_chunk[seg];
+        if (p.fast) {
+            const std::int64_t beg = j * kPushChunk, end = i64min(p.units, beg + kPushChunk);
+            std::int64_t u = beg + threadIdx.x;
+            if (end - beg == kPushChunk) {
+                float4 g[kPushUnroll];
+#pragma unroll
+                for (int k = 0; k < kPushUnroll; ++k) g[k] = load_grad4<BF16>(src, p.head + 4 * (u + k * kPushThreads));
+#pragma unroll
+                for (int k = 0; k < kPushUnroll; ++k)
+                    red_sys_v4(dst + p.head + 4 * (u + k * kPushThreads), __fmul_rn(w, g[k].x), __fmul_rn(w, g[k].y),
+                               __fmul_rn(w, g[k].z), __fmul_rn(w, g[k].w));
+            } else {
+                for (; u < end; u += kPushThreads) {
+                    const float4 g = load_grad4<BF16>(src, p.head + 4 * u);
+                    red_sys_v4(dst + p.head + 4 * u, __fmul_rn(w, g.x), __fmul_rn(w, g.y), __fmul_rn(w, g.z),
+                               __fmul_rn(w, g.w));
+                }
+            }
+            if (j == 0) {
+                if (threadIdx.x < p.head) red_sys_f32(dst + threadIdx.x, __fmul_rn(w, load_grad<BF16>(src, threadIdx.x)));
+                const std::int64_t tb = p.head + 4 * p.units;
+                if (threadIdx.x < p.tail)
+                    red_sys_f32(dst + tb + threadIdx.x, __fmul_rn(w, load_grad<BF16>(src, tb + threadIdx.x)));
+            }
+        } else {
+            const std::int64_t beg = j * kPushChunk * 4, end = i64min(t.elems[seg], beg + kPushChunk * 4);
+            for (std::int64_t e = beg + threadIdx.x; e < end; e += kPushThreads)
+                red_sys_f32(dst + e, __fmul_rn(w, load_grad<BF16>(src, e)));
+        }
+    }
+}
+
+cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas, cudaStream_t s) {
+    if (t.n <= 0) return cudaSuccess;
+    if (ctas <= 0) ctas = 148;
+    count_launch();
+    if (src_bf16) push_red_kernel<true><<<ctas, kPushThreads, 0, s>>>(t, w);
+    else push_red_kernel<false><<<ctas, kPushThreads, 0, s>>>(t, w);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ push (SLOT)
+struct GateList {
+    const unsigned long long* g[kMaxSeg];
+    int n;
+    unsigned long long need;
+    unsigned long long* err;
+    long long timeout_ns;
+};
+
+__device__ __forceinline__ bool pass_gates(const GateList& gl) {
+    __shared__ int ok;
+    if (threadIdx.x == 0) ok = 1;
+    __syncthreads();
+    if (threadIdx.x < gl.n && !wait_geq(gl.g[threadIdx.x], gl.need, gl.err, gl.timeout_ns)) ok = 0;
+    __syncthreads();
+    return ok != 0;
+}
+
+template <bool BF16, bool ASSIGN>
+__global__ void __launch_bounds__(512) slot_accumulate_kernel(float* __restrict__ acc, const void* __restrict__ grad,
+                                                               std::int64_t n, float w, GateList gl) {
+    if (gl.n > 0 && !pass_gates(gl)) return;
+    // acc and grad are both 16B/8B aligned at element 0 (full-layer buffers)
+    const std::int64_t units = n / 4;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < units; u += stride) {
+        const float4 g = load_grad4<BF16>(grad, 4 * u);
+        float4 a = ASSIGN ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4*>(acc)[u];
+        a.x = __fadd_rn(a.x, __fmul_rn(w, g.x));
+        a.y = __fadd_rn(a.y, __fmul_rn(w, g.y));
+        a.z = __fadd_rn(a.z, __fmul_rn(w, g.z));
+        a.w = __fadd_rn(a.w, __fmul_rn(w, g.w));
+        reinterpret_cast<float4*>(acc)[u] = a;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < n - 4 * units) {
+        const std::int64_t e = 4 * units + threadIdx.x;
+        acc[e] = __fadd_rn(ASSIGN ? 0.f : acc[e], __fmul_rn(w, load_grad<BF16>(grad, e)));
+    }
+}
+
+cudaError_t launch_slot_accumulate(float* acc, const void* grad, bool src_bf16, std::int64_t n, float w, bool assign,
+                                   const unsigned long long* const* gates, int ngates, unsigned long long need,
+                                   unsigned long long* err, long long timeout_ns, int ctas, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (reinterpret_cast<uintptr_t>(acc) % 16 || reinterpret_cast<uintptr_t>(grad) % (src_bf16 ? 8 : 16))
+        return cudaErrorMisalignedAddress;
+    GateList gl{};
+    gl.n = ngates;
+    for (int i = 0; i < ngates; ++i) gl.g[i] = gates[i];
+    gl.need = need;
+    gl.err = err;
+    gl.timeout_ns = timeout_ns;
+    if (ctas <= 0) ctas = 296;
+    count_launch();
+    if (src_bf16) {
+        if (assign) slot_accumulate_kernel<true, true><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
+        else slot_accumulate_kernel<true, false><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
+    } else {
+        if (assign) slot_accumulate_kernel<false, true><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
+        else slot_accumulate_kernel<false, false><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
+    }
+    return cudaGetLastError();
+}
+
+// owner-side fixed-order reduce of the per-source slots (peer loads)
+struct SrcList {
+    const float* p[kMaxSeg];
+    int n;
+};
+
+__global__ void __launch_bounds__(512) reduce_sources_kernel(float* __restrict__ dst, SrcList sl, std::int64_t n) {
+    // dst and every source are co-aligned (same element offset mod 4)
+    const unsigned h = static_cast<unsigned>((reinterpret_cast<uintptr_t>(dst) >> 2) & 3);
+    const std::int64_t head = i64min(n, (4 - h) & 3);
+    const std::int64_t units = (n - head) / 4;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < units; u += stride) {
+        const std::int64_t e = head + 4 * u;
+        float4 a = *reinterpret_cast<const float4*>(sl.p[0] + e);
+        for (int c = 1; c < sl.n; ++c) {  // rank order 0..N-1: deterministic
+            const float4 b = *reinterpret_cast<const float4*>(sl.p[c] + e);
+            a.x = __fadd_rn(a.x, b.x);
+            a.y = __fadd_rn(a.y, b.y);
+            a.z = __fadd_rn(a.z, b.z);
+            a.w = __fadd_rn(a.w, b.w);
+        }
+        *reinterpret_cast<float4*>(dst + e) = a;
+    }
+    if (blockIdx.x == 0) {
+        const std::int64_t tail = n - head - 4 * units;
+        int e = -1;
+        if (threadIdx.x < head) e = threadIdx.x;
+        else if (threadIdx.x >= 4 && threadIdx.x < 4 + tail) e = static_cast<int>(head + 4 * units + threadIdx.x - 4);
+        if (e >= 0) {
+            float a = sl.p[0][e];
+            for (int c = 1; c < sl.n; ++c) a = __fadd_rn(a, sl.p[c][e]);
+            dst[e] = a;
+        }
+    }
+}
+
+cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc, std::int64_t n, int ctas,
+                                  cudaStream_t s) {
+    if (n <= 0 || nsrc <= 0) return cudaSuccess;
+    SrcList sl{};
+    sl.n = nsrc;
+    for (int i = 0; i < nsrc; ++i) sl.p[i] = srcs[i];
+    if (ctas <= 0) ctas = 296;
+    count_launch();
+    reduce_sources_kernel<<<ctas, 512, 0, s>>>(dst, sl, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------ typed fabric accumulate
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b) { return a * b; }
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b) { return a + b; }
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T>
+__global__ void accumulate_kernel(T* __restrict__ dst, const T* __restrict__ src, std::int64_t n, T w) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = add_rn(dst[i], mul_rn(w, src[i]));
+}
+
+template <typename T>
+__device__ __forceinline__ void red_one(T* p, T v);
+template <>
+__device__ __forceinline__ void red_one<long long>(long long* p, long long v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <>
+__device__ __forceinline__ void red_one<double>(double* p, double v) {
+    asm volatile("red.relaxed.sys.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+template <>
+__device__ __forceinline__ void red_one<float>(float* p, float v) {
+    red_sys_f32(p, v);
+}
+
+template <typename T>
+__global__ void red_accumulate_kernel(T* __restrict__ dst, const T* __restrict__ src, std::int64_t n, T w) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        red_one<T>(dst + i, mul_rn(w, src[i]));
+}
+
+static int small_grid(std::int64_t n) {
+    std::int64_t g = (n + 255) / 256;
+    return static_cast<int>(g < 1 ? 1 : (g > 592 ? 592 : g));
+}
+
+template <typename T>
+cudaError_t launch_accumulate(T* dst, const T* src, std::int64_t n, T w, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    count_launch();
+    accumulate_kernel<T><<<small_grid(n), 256, 0, s>>>(dst, src, n, w);
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_red_accumulate(T* dst, const T* src, std::int64_t n, T w, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    count_launch();
+    red_accumulate_kernel<T><<<small_grid(n), 256, 0, s>>>(dst, src, n, w);
+    return cudaGetLastError();
+}
+template cudaError_t launch_accumulate<long long>(long long*, const long long*, std::int64_t, long long, cudaStream_t);
+template cudaError_t launch_accumulate<double>(double*, const double*, std::int64_t, double, cudaStream_t);
+template cudaError_t launch_accumulate<float>(float*, const float*, std::int64_t, float, cudaStream_t);
+template cudaError_t launch_red_accumulate<long long>(long long*, const long long*, std::int64_t, long long,
+                                                      cudaStream_t);
+template cudaError_t launch_red_accumulate<double>(double*, const double*, std::int64_t, double, cudaStream_t);
+template cudaError_t launch_red_accumulate<float>(float*, const float*, std::int64_t, float, cudaStream_t);
+
+// ------------------------------------------------------------- barrier
+__global__ void barrier_kernel(BarrierArgs a) {
+    const int t = threadIdx.x;
+    if (t < a.world) {
+        // release: every push this rank issued earlier on the stream (kernel
+        // boundaries order them before this thread) is visible to owner t
+        // before it observes the flag. PTX release is cumulative.
+        st_release_sys(a.peer_done[t] + a.rank, a.epoch);
+    }
+    if (t < a.world) wait_geq(a.my_done + t, a.epoch, a.err, a.timeout_ns);
+    __syncthreads();
+}
+
+cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
+    count_launch();
+    barrier_kernel<<<1, 32 * ((a.world + 31) / 32), 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void publish_kernel(unsigned long long* flag, unsigned long long v) { st_release_sys(flag, v); }
+
+cudaError_t launch_publish(unsigned long long* flag, unsigned long long value, cudaStream_t s) {
+    count_launch();
+    publish_kernel<<<1, 1, 0, s>>>(flag, value);
+    return cudaGetLastError();
+}
+
+struct ZeroList {
+    float* p[64];
+    std::int64_t n[64];
+    int count;
+};
+
+__global__ void gated_zero_kernel(ZeroList z, GateList gl) {
+    if (gl.n > 0 && !pass_gates(gl)) return;
+    for (int k = 0; k < z.count; ++k) {
+        const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+        for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < z.n[k]; i += stride)
+            z.p[k][i] = 0.f;
+    }
+}
+
+cudaError_t launch_gated_zero(float* const* ptrs, const std::int64_t* n, int count,
+                              const unsigned long long* const* gates, int ngates, unsigned long long need,
+                              unsigned long long* err, long long timeout_ns, cudaStream_t s) {
+    GateList gl{};
+    gl.n = ngates;
+    for (int i = 0; i < ngates; ++i) gl.g[i] = gates[i];
+    gl.need = need;
+    gl.err = err;
+    gl.timeout_ns = timeout_ns;
+    for (int base = 0; base < count; base += 64) {
+        ZeroList z{};
+        z.count = count - base < 64 ? count - base : 64;
+        for (int k = 0; k < z.count; ++k) {
+            z.p[k] = ptrs[base + k];
+            z.n[k] = n[base + k];
+        }
+        count_launch();
+        gated_zero_kernel<<<296, 512, 0, s>>>(z, gl);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- AdamW
+// torch.optim.AdamW(foreach=False) update order:
+//   p *= 1 - lr*wd;  m = lerp(m, g, 1-b1);  v = b2*v + (1-b2)*g*g
+//   p -= step_size * m / (sqrt(v)/sqrt(bc2) + eps)
+__device__ __forceinline__ void adam_one(float& p, float& m, float& v, float g, const AdamArgs& a) {
+    p = p * (1.f - a.lr * a.wd);
+    m = m + (1.f - a.beta1) * (g - m);
+    v = a.beta2 * v + (1.f - a.beta2) * g * g;
+    const float denom = sqrtf(v) * a.bc2_sqrt_inv + a.eps;
+    p = p - a.step_size * (m / denom);
+}
+
+__global__ void __launch_bounds__(512) adam_kernel(AdamArgs a) {
+    const std::int64_t total = a.seg_start[a.nseg];
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    int seg = 0;
+    for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total; u += stride) {
+        while (u >= a.seg_start[seg + 1]) ++seg;
+        const AdamSeg S = a.segs[seg];
+        // unit k covers elements [4k - h, 4k - h + 4) of the shard, where h
+        // is the shard's element offset mod 4 (all fp32 arrays co-aligned)
+        const int h = static_cast<int>((reinterpret_cast<uintptr_t>(S.master) >> 2) & 3);
+        const std::int64_t k = u - a.seg_start[seg];
+        const std::int64_t e0 = 4 * k - h;
+        if (e0 >= 0 && e0 + 4 <= S.n) {
+            float4 p = *reinterpret_cast<float4*>(S.master + e0);
+            float4 m = *reinterpret_cast<float4*>(S.m + e0);
+            float4 v = *reinterpret_cast<float4*>(S.v + e0);
+            float4 g = *reinterpret_cast<float4*>(S.grad + e0);
+            adam_one(p.x, m.x, v.x, g.x, a);
+            adam_one(p.y, m.y, v.y, g.y, a);
+            adam_one(p.z, m.z, v.z, g.z, a);
+            adam_one(p.w, m.w, v.w, g.w, a);
+            *reinterpret_cast<float4*>(S.master + e0) = p;
+            *reinterpret_cast<float4*>(S.m + e0) = m;
+            *reinterpret_cast<float4*>(S.v + e0) = v;
+            *reinterpret_cast<float4*>(S.grad + e0) = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint2 pb;
+            pb.x = static_cast<unsigned>(f32_to_bf16(p.x)) | (static_cast<unsigned>(f32_to_bf16(p.y)) << 16);
+            pb.y = static_cast<unsigned>(f32_to_bf16(p.z)) | (static_cast<unsigned>(f32_to_bf16(p.w)) << 16);
+            *reinterpret_cast<uint2*>(S.param + e0) = pb;
+        } else {
+            for (std::int64_t e = e0 < 0 ? 0 : e0; e < e0 + 4 && e < S.n; ++e) {
+                float p = S.master[e], m = S.m[e], v = S.v[e];
+                adam_one(p, m, v, S.grad[e], a);
+                S.master[e] = p;
+                S.m[e] = m;
+                S.v[e] = v;
+                S.grad[e] = 0.f;
+                S.param[e] = f32_to_bf16(p);
+            }
+        }
+    }
+}
+
+cudaError_t launch_adam(const AdamArgs& a, std::int64_t total_units, int ctas, cudaStream_t s) {
+    if (total_units <= 0) return cudaSuccess;
+    if (ctas <= 0) ctas = 148 * 4;
+    count_launch();
+    adam_kernel<<<ctas, 512, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ L2 flush
+__global__ void l2_flush_kernel(uint4* p, std::int64_t n) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        p[i] = make_uint4(static_cast<unsigned>(i), 0u, 0u, 0u);
+}
+
+cudaError_t launch_l2_flush(void* scratch, std::int64_t bytes, cudaStream_t s) {
+    count_launch();
+    l2_flush_kernel<<<148 * 2, 512, 0, s>>>(reinterpret_cast<uint4*>(scratch), bytes / 16);
+    return cudaGetLastError();
+}
+
+__global__ void init_shard_kernel(float* master, unsigned short* param, const float* src, std::int64_t n) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float x = src[i];
+        master[i] = x;
+        param[i] = f32_to_bf16(x);
+    }
+}
+
+cudaError_t launch_init_shard(float* master, unsigned short* param, const float* src, std::int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    count_launch();
+    init_shard_kernel<<<296, 512, 0, s>>>(master, param, src, n);
+    return cudaGetLastError();
+}
+
+}  // namespace odc

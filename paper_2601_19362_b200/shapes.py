@@ -1,0 +1,51 @@
+"""Model shapes of the BASELINE configs (public HF configs)
+and the FSDP-unit element counts the ODC shard store is sized from."""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Shape:
+    name: str
+    d: int
+    ffn: int
+    layers: int
+    heads: int
+    kv_heads: int
+    vocab: int
+    qkv_bias: bool
+    tied: bool
+
+    @property
+    def head_dim(self) -> int:
+        return self.d // self.heads
+
+    @property
+    def layer_elems(self) -> int:
+        """Elements of one transformer layer = one FSDP unit:
+        q, k, v (+bias), o, gate/up/down, 2 RMSNorm weights."""
+        hd = self.head_dim
+        q = self.d * self.d + (self.d if self.qkv_bias else 0)
+        kv = 2 * (self.kv_heads * hd * self.d + (self.kv_heads * hd if self.qkv_bias else 0))
+        o = self.d * self.d
+        mlp = 3 * self.d * self.ffn
+        return q + kv + o + mlp + 2 * self.d
+
+    @property
+    def nonembed_params(self) -> int:
+        return self.layers * self.layer_elems + self.d  # + final norm
+
+    def beta_over_alpha(self) -> float:
+        """Cost-model beta/alpha = P_nonembed / (n_layer * d)."""
+        return self.nonembed_params / (self.layers * self.d)
+
+
+QWEN25_1_5B = Shape("qwen2.5-1.5b", 1536, 8960, 28, 12, 2, 151936, True, True)
+LLAMA3_8B = Shape("llama-3-8b", 4096, 14336, 32, 32, 8, 128256, False, False)
+QWEN25_14B = Shape("qwen2.5-14b", 5120, 13824, 48, 40, 8, 152064, True, False)
+SHAPES = {s.name: s for s in (QWEN25_1_5B, LLAMA3_8B, QWEN25_14B)}
+
+assert QWEN25_1_5B.layer_elems == 46_797_824
+assert LLAMA3_8B.layer_elems == 218_112_000
+assert QWEN25_14B.layer_elems == 275_268_608
