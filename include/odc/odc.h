@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ODC_ABI_VERSION 1
+#define ODC_ABI_VERSION 2
 
 typedef enum {
     ODC_OK = 0,
@@ -122,7 +122,14 @@ typedef struct {
     int fetch_ctas;             /* CTAs for fetch (0 = default): non-intrusive SM budget */
     int push_ctas;              /* CTAs for push  (0 = default) */
     double timeout_s;           /* device barrier watchdog (<= 0: 60 s) */
+    int fetch_engine;           /* odc_fetch_engine */
 } odc_config;
+
+typedef enum {
+    ODC_FETCH_TMA = 0, /* sm_100a kernel: cp.async.bulk peer->smem->local pipeline (default) */
+    ODC_FETCH_LDG = 1, /* sm_100a kernel: 16-byte vector peer loads, chunked */
+    ODC_FETCH_CE = 2   /* copy engines (cudaMemcpyAsync per owner) after a device gate kernel */
+} odc_fetch_engine;
 
 odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out);
 odc_status odc_ctx_destroy(odc_ctx_t ctx);

@@ -135,6 +135,25 @@ odc_ctx* C(odc_ctx_t c) {
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// fetch engine dispatch (odc_fetch_engine)
+void launch_fetch(const odc_ctx* c, const odc::SegTable& t, cudaStream_t s) {
+    switch (c->cfg.fetch_engine) {
+        case ODC_FETCH_LDG: cuda_ok(odc::launch_copy_segments(t, c->cfg.fetch_ctas, s), "fetch (ldg)"); return;
+        case ODC_FETCH_CE: {
+            const unsigned long long* gates[odc::kMaxSeg];
+            for (int i = 0; i < t.n; ++i) gates[i] = t.gate[i];
+            cuda_ok(odc::launch_gated_zero(nullptr, nullptr, 0, gates, t.n, t.need, t.err, t.timeout_ns, s), "gate");
+            for (int i = 0; i < t.n; ++i)
+                if (t.bytes[i] > 0)
+                    cuda_ok(cudaMemcpyAsync(t.dst[i], t.src[i], static_cast<std::size_t>(t.bytes[i]),
+                                            cudaMemcpyDeviceToDevice, s),
+                            "fetch (ce)");
+            return;
+        }
+        default: cuda_ok(odc::launch_fetch_tma(t, c->cfg.fetch_ctas, s), "fetch (tma)");
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -161,6 +180,7 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
         if (cfg->rank < 0 || cfg->rank >= cfg->world) throw ParamError("rank out of range");
         if (cfg->n_layers < 1 || !cfg->layer_elems) throw ParamError("need at least one FSDP unit");
         if (cfg->push_mode != ODC_PUSH_RED && cfg->push_mode != ODC_PUSH_SLOT) throw ParamError("bad push mode");
+        if (cfg->fetch_engine < ODC_FETCH_TMA || cfg->fetch_engine > ODC_FETCH_CE) throw ParamError("bad fetch engine");
         auto* c = new odc_ctx();
         try {
             c->cfg = *cfg;
@@ -330,7 +350,7 @@ odc_status odc_fetch(odc_ctx_t ch, int layer, void* dst_full, void* stream) {
         t.need = c->adams;
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
-        cuda_ok(odc::launch_copy_segments(t, c->cfg.fetch_ctas, S(stream)), "fetch");
+        launch_fetch(c, t, S(stream));
     });
 }
 
@@ -352,7 +372,7 @@ odc_status odc_fetch_master(odc_ctx_t ch, int layer, float* dst_full, void* stre
         t.need = c->adams;
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
-        cuda_ok(odc::launch_copy_segments(t, c->cfg.fetch_ctas, S(stream)), "fetch_master");
+        launch_fetch(c, t, S(stream));
     });
 }
 

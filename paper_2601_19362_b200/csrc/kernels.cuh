@@ -42,6 +42,9 @@ std::uint64_t launches();
 void count_launch();
 
 cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s);
+// fetch engine: TMA bulk peer->smem->local pipeline, every CTA round-robins a
+// slice of every segment (all owners served concurrently)
+cudaError_t launch_fetch_tma(const SegTable& t, int ctas, cudaStream_t s);
 // push, RED mode: remote red.relaxed.sys.global.add(.v4).f32 into owner shards
 cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas, cudaStream_t s);
 // push, SLOT mode (deterministic, local): acc[i] = (assign ? 0 : acc[i]) + w*g[i]

@@ -184,6 +184,169 @@ cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------- fetch (TMA bulk)
+// The fetch engine proper. One elected thread per CTA streams chunks
+// peer HBM --cp.async.bulk--> smem --cp.async.bulk--> local HBM through a
+// kTmaStages-deep mbarrier pipeline, so each CTA keeps ~96 KB of NVLink reads
+// in flight from a single thread; a small CTA budget leaves the SMs to the
+// model's kernels. Every CTA owns a contiguous slice of EVERY owner's shard
+// and walks the slices round-robin, so all owners (and the local shard) are
+// served concurrently instead of one after the other. Bytes before the first
+// 16-byte-aligned address and after the last one (ragged shards) are moved
+// by a second warp.
+constexpr int kTmaChunk = 32768;
+constexpr int kTmaStages = 4;
+constexpr int kTmaThreads = 64;
+constexpr int kTmaSmem = kTmaChunk * kTmaStages;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+struct TmaJobs {
+    // this CTA's slice of every segment, in 16-byte-aligned body chunks
+    std::int64_t first[kMaxSeg], count[kMaxSeg], body0[kMaxSeg], body_bytes[kMaxSeg];
+    int n;
+    std::int64_t k;  // round
+    int s;           // segment within the round
+    __device__ bool next(int& seg, std::int64_t& off, int& bytes) {
+        std::int64_t maxc = 0;
+        for (int i = 0; i < n; ++i) maxc = count[i] > maxc ? count[i] : maxc;
+        while (k < maxc) {
+            while (s < n) {
+                const int i = s++;
+                if (k < count[i]) {
+                    const std::int64_t c = first[i] + k;
+                    seg = i;
+                    off = body0[i] + c * kTmaChunk;
+                    const std::int64_t rem = body0[i] + body_bytes[i] - off;
+                    bytes = static_cast<int>(rem < kTmaChunk ? rem : kTmaChunk);
+                    return true;
+                }
+            }
+            s = 0;
+            ++k;
+        }
+        return false;
+    }
+};
+
+__global__ void __launch_bounds__(kTmaThreads, 1) fetch_tma_kernel(SegTable t) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ __align__(8) unsigned long long bar[kTmaStages];
+    __shared__ int gate_ok;
+    const int tid = threadIdx.x;
+    if (tid == 0) gate_ok = 1;
+    __syncthreads();
+    // on-demand readiness: every owner published the parameter epoch we need
+    if (tid < t.n && t.gate[tid] && !wait_geq(t.gate[tid], t.need, t.err, t.timeout_ns)) gate_ok = 0;
+    __syncthreads();
+    if (!gate_ok) return;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+
+    if (tid >= 32) {  // warp 1: ragged head/tail bytes and non-co-aligned segments
+        const int lane = tid - 32;
+        for (int i = 0; i < t.n; ++i) {
+            const char* src = t.src[i];
+            char* dst = t.dst[i];
+            const std::int64_t bytes = t.bytes[i];
+            if (bytes <= 0) continue;
+            const unsigned sa = static_cast<unsigned>(reinterpret_cast<uintptr_t>(src) & 15);
+            const unsigned da = static_cast<unsigned>(reinterpret_cast<uintptr_t>(dst) & 15);
+            if (sa != da) {  // slow path: this CTA's byte slice
+                const std::int64_t b0 = bytes * blockIdx.x / gridDim.x, b1 = bytes * (blockIdx.x + 1) / gridDim.x;
+                for (std::int64_t b = b0 + lane; b < b1; b += 32) dst[b] = src[b];
+                continue;
+            }
+            if (blockIdx.x != 0) continue;
+            const std::int64_t head = i64min(bytes, (16 - da) & 15);
+            const std::int64_t body = (bytes - head) & ~static_cast<std::int64_t>(15);
+            if (lane < head) dst[lane] = src[lane];
+            const std::int64_t tb = head + body;
+            if (lane < bytes - tb) dst[tb + lane] = src[tb + lane];
+        }
+        return;
+    }
+    if (tid != 0) return;
+
+    TmaJobs jobs{};
+    jobs.n = t.n;
+    for (int i = 0; i < t.n; ++i) {
+        const std::int64_t bytes = t.bytes[i];
+        const unsigned sa = static_cast<unsigned>(reinterpret_cast<uintptr_t>(t.src[i]) & 15);
+        const unsigned da = static_cast<unsigned>(reinterpret_cast<uintptr_t>(t.dst[i]) & 15);
+        if (bytes <= 0 || sa != da) {
+            jobs.count[i] = 0;
+            continue;
+        }
+        const std::int64_t head = i64min(bytes, (16 - da) & 15);
+        jobs.body0[i] = head;
+        jobs.body_bytes[i] = (bytes - head) & ~static_cast<std::int64_t>(15);
+        const std::int64_t nch = (jobs.body_bytes[i] + kTmaChunk - 1) / kTmaChunk;
+        jobs.first[i] = nch * blockIdx.x / gridDim.x;
+        jobs.count[i] = nch * (blockIdx.x + 1) / gridDim.x - jobs.first[i];
+    }
+    for (int s = 0; s < kTmaStages; ++s)
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+    int seg[kTmaStages], nbytes[kTmaStages];
+    std::int64_t off[kTmaStages];
+    unsigned phase = 0;  // bit s = parity to wait for on stage s
+    auto load = [&](int st) {
+        const unsigned b = smem_u32(&bar[st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(b), "r"(nbytes[st]) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(smem + st * kTmaChunk)),
+            "l"(t.src[seg[st]] + off[st]), "r"(nbytes[st]), "r"(b)
+            : "memory");
+    };
+    int inflight = 0;
+    for (int st = 0; st < kTmaStages; ++st) {
+        if (!jobs.next(seg[st], off[st], nbytes[st])) break;
+        load(st);
+        ++inflight;
+    }
+    for (int j = 0; inflight > 0; ++j) {
+        const int st = j % kTmaStages;
+        asm volatile(
+            "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
+                smem_u32(&bar[st])),
+            "r"((phase >> st) & 1u)
+            : "memory");
+        phase ^= 1u << st;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(t.dst[seg[st]] + off[st]),
+                     "r"(smem_u32(smem + st * kTmaChunk)), "r"(nbytes[st])
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        --inflight;
+        if (jobs.next(seg[st], off[st], nbytes[st])) {
+            // the stage's smem may be refilled once the store has read it
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            load(st);
+            ++inflight;
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+cudaError_t launch_fetch_tma(const SegTable& t, int ctas, cudaStream_t s) {
+    if (t.n <= 0) return cudaSuccess;
+    static thread_local int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(fetch_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+        if (e != cudaSuccess) return e;
+        configured_dev = dev;
+    }
+    if (ctas <= 0) ctas = 64;
+    count_launch();
+    fetch_tma_kernel<<<ctas, kTmaThreads, kTmaSmem, s>>>(t);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- push (RED)
 constexpr int kPushThreads = 512;
 constexpr int kPushUnroll = 4;
@@ -231,63 +394,68 @@ __device__ __forceinline__ float4 load_grad4(const void* src, std::int64_t e) {
 
 template <bool BF16>
 __global__ void __launch_bounds__(kPushThreads) push_red_kernel(RedTable t, float w) {
+    // Every CTA owns a contiguous slice of every owner's shard and walks the
+    // slices round-robin in kPushChunk-unit steps, so all owners (and the
+    // local shard) receive reductions concurrently.
     __shared__ RedPlan plans[kMaxSeg];
-    __shared__ std::int64_t first_chunk[kMaxSeg + 1];
+    __shared__ std::int64_t lo[kMaxSeg], hi[kMaxSeg];
     __shared__ int gate_ok;
-    if (threadIdx.x == 0) {
-        std::int64_t acc = 0;
-        for (int i = 0; i < t.n; ++i) {
-            plans[i] = plan_red(t.src[i], t.dst[i], t.elems[i], BF16);
-            first_chunk[i] = acc;
-            acc += plans[i].chunks;
-        }
-        first_chunk[t.n] = acc;
+    if (threadIdx.x == 0) gate_ok = 1;
+    __syncthreads();
+    // the owner finished its previous AdamW (its grad shard is zeroed)
+    if (threadIdx.x < t.n && t.gate[threadIdx.x] && !wait_geq(t.gate[threadIdx.x], t.need, t.err, t.timeout_ns))
+        gate_ok = 0;
+    if (threadIdx.x < t.n) {
+        const int i = threadIdx.x;
+        RedPlan p = plan_red(t.src[i], t.dst[i], t.elems[i], BF16);
+        plans[i] = p;
+        const std::int64_t n = p.fast ? p.units : t.elems[i];  // units of 4 (fast) or elements (slow)
+        lo[i] = n * blockIdx.x / gridDim.x;
+        hi[i] = n * (blockIdx.x + 1) / gridDim.x;
     }
     __syncthreads();
-    const std::int64_t total = first_chunk[t.n];
-    int seg = 0, gated_seg = -1;
-    for (std::int64_t c = blockIdx.x; c < total; c += gridDim.x) {
-        while (c >= first_chunk[seg + 1]) ++seg;
-        if (t.gate[seg] && gated_seg != seg) {  // owner finished its previous Adam step
-            if (threadIdx.x == 0) gate_ok = wait_geq(t.gate[seg], t.need, t.err, t.timeout_ns);
-            __syncthreads();
-            const bool ok = gate_ok != 0;
-            __syncthreads();  // gate_ok may be rewritten at the next segment switch
-            gated_seg = seg;
-            if (!ok) continue;
-        }
-        const RedPlan p = plans[seg];
-        const void* src = t.src[seg];
-        float* dst = t.dst[seg];
-        const std::int64_t j = c - first_chunk[seg];
-        if (p.fast) {
-            const std::int64_t beg = j * kPushChunk, end = i64min(p.units, beg + kPushChunk);
-            std::int64_t u = beg + threadIdx.x;
-            if (end - beg == kPushChunk) {
-                float4 g[kPushUnroll];
+    if (!gate_ok) return;
+    std::int64_t maxlen = 0;
+    for (int i = 0; i < t.n; ++i) maxlen = i64max(maxlen, hi[i] - lo[i]);
+    for (std::int64_t k = 0; k < maxlen; k += kPushChunk) {
+        for (int i = 0; i < t.n; ++i) {
+            const std::int64_t beg = lo[i] + k;
+            const std::int64_t end = i64min(hi[i], beg + kPushChunk);
+            if (beg >= end) continue;
+            const RedPlan p = plans[i];
+            const void* src = t.src[i];
+            float* dst = t.dst[i];
+            if (p.fast) {
+                std::int64_t u = beg + threadIdx.x;
+                if (end - beg == kPushChunk) {
+                    float4 g[kPushUnroll];
 #pragma unroll
-                for (int k = 0; k < kPushUnroll; ++k) g[k] = load_grad4<BF16>(src, p.head + 4 * (u + k * kPushThreads));
+                    for (int q = 0; q < kPushUnroll; ++q) g[q] = load_grad4<BF16>(src, p.head + 4 * (u + q * kPushThreads));
 #pragma unroll
-                for (int k = 0; k < kPushUnroll; ++k)
-                    red_sys_v4(dst + p.head + 4 * (u + k * kPushThreads), __fmul_rn(w, g[k].x), __fmul_rn(w, g[k].y),
-                               __fmul_rn(w, g[k].z), __fmul_rn(w, g[k].w));
-            } else {
-                for (; u < end; u += kPushThreads) {
-                    const float4 g = load_grad4<BF16>(src, p.head + 4 * u);
-                    red_sys_v4(dst + p.head + 4 * u, __fmul_rn(w, g.x), __fmul_rn(w, g.y), __fmul_rn(w, g.z),
-                               __fmul_rn(w, g.w));
+                    for (int q = 0; q < kPushUnroll; ++q)
+                        red_sys_v4(dst + p.head + 4 * (u + q * kPushThreads), __fmul_rn(w, g[q].x), __fmul_rn(w, g[q].y),
+                                   __fmul_rn(w, g[q].z), __fmul_rn(w, g[q].w));
+                } else {
+                    for (; u < end; u += kPushThreads) {
+                        const float4 g = load_grad4<BF16>(src, p.head + 4 * u);
+                        red_sys_v4(dst + p.head + 4 * u, __fmul_rn(w, g.x), __fmul_rn(w, g.y), __fmul_rn(w, g.z),
+                                   __fmul_rn(w, g.w));
+                    }
                 }
+            } else {
+                for (std::int64_t e = beg + threadIdx.x; e < end; e += kPushThreads)
+                    red_sys_f32(dst + e, __fmul_rn(w, load_grad<BF16>(src, e)));
             }
-            if (j == 0) {
-                if (threadIdx.x < p.head) red_sys_f32(dst + threadIdx.x, __fmul_rn(w, load_grad<BF16>(src, threadIdx.x)));
-                const std::int64_t tb = p.head + 4 * p.units;
-                if (threadIdx.x < p.tail)
-                    red_sys_f32(dst + tb + threadIdx.x, __fmul_rn(w, load_grad<BF16>(src, tb + threadIdx.x)));
-            }
-        } else {
-            const std::int64_t beg = j * kPushChunk * 4, end = i64min(t.elems[seg], beg + kPushChunk * 4);
-            for (std::int64_t e = beg + threadIdx.x; e < end; e += kPushThreads)
-                red_sys_f32(dst + e, __fmul_rn(w, load_grad<BF16>(src, e)));
+        }
+    }
+    if (blockIdx.x == 0) {  // ragged head / tail elements of the fast segments
+        for (int i = 0; i < t.n; ++i) {
+            const RedPlan p = plans[i];
+            if (!p.fast) continue;
+            if (threadIdx.x < p.head) red_sys_f32(t.dst[i] + threadIdx.x, __fmul_rn(w, load_grad<BF16>(t.src[i], threadIdx.x)));
+            const std::int64_t tb = p.head + 4 * p.units;
+            if (threadIdx.x < p.tail)
+                red_sys_f32(t.dst[i] + tb + threadIdx.x, __fmul_rn(w, load_grad<BF16>(t.src[i], tb + threadIdx.x)));
         }
     }
 }
@@ -535,6 +703,12 @@ cudaError_t launch_gated_zero(float* const* ptrs, const std::int64_t* n, int cou
     gl.need = need;
     gl.err = err;
     gl.timeout_ns = timeout_ns;
+    if (count == 0) {  // gate only (copy-engine fetch waits on it in stream order)
+        ZeroList z{};
+        count_launch();
+        gated_zero_kernel<<<1, 32, 0, s>>>(z, gl);
+        return cudaGetLastError();
+    }
     for (int base = 0; base < count; base += 64) {
         ZeroList z{};
         z.count = count - base < 64 ? count - base : 64;

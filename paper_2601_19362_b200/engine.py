@@ -27,6 +27,7 @@ from . import _lib
 from ._lib import check, lib
 
 PUSH_MODES = {"red": _lib.ODC_PUSH_RED, "slot": _lib.ODC_PUSH_SLOT}
+FETCH_ENGINES = {"tma": _lib.ODC_FETCH_TMA, "ldg": _lib.ODC_FETCH_LDG, "ce": _lib.ODC_FETCH_CE}
 
 
 def _stream(stream: Optional[torch.cuda.Stream]):
@@ -45,14 +46,14 @@ def _ptr(t: torch.Tensor):
 class OdcEngine:
     def __init__(self, layer_elems: Sequence[int], rank: int = 0, world: int = 1, device: Optional[int] = None,
                  push_mode: str = "red", fetch_ctas: int = 0, push_ctas: int = 0, timeout_s: float = 60.0,
-                 group=None):
+                 group=None, fetch_engine: str = "tma"):
         self.layer_elems = [int(x) for x in layer_elems]
         self.rank, self.world = rank, world
         self.device = torch.cuda.current_device() if device is None else device
         self.push_mode = push_mode
         arr = (C.c_int64 * len(self.layer_elems))(*self.layer_elems)
         cfg = _lib.OdcConfig(rank, world, self.device, len(self.layer_elems), arr, PUSH_MODES[push_mode], fetch_ctas,
-                             push_ctas, timeout_s)
+                             push_ctas, timeout_s, FETCH_ENGINES[fetch_engine])
         h = C.c_void_p()
         check(lib().odc_ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h
