@@ -186,6 +186,21 @@ odc_status odc_copy_segments(int nseg, const void* const* srcs, void* const* dst
 odc_status odc_l2_flush(void* scratch, int64_t bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * bf16 GEMM on tcgen05 tensor cores (worker dense layers; no reference
+ * counterpart — the reference only models their cost, src/cost_model.cpp).
+ *   D[M,N] (+)= A · B^T with fp32 accumulation in TMEM
+ *   A stored [M][K] (a_mn_major = 0) or [K][M] (a_mn_major = 1), pitch lda
+ *   B stored [N][K] (b_mn_major = 0) or [K][N] (b_mn_major = 1), pitch ldb
+ *   D row-major [M][ldd], d_dtype ODC_BF16 or ODC_F32; accumulate: D += A·B^T
+ * fwd  X·W^T : a=X [T][in] K-major,  b=W [out][in] K-major
+ * dgrad dY·W : a=dY [T][out] K-major, b=W [out][in] N-major
+ * wgrad dY^T·X: a=dY [T][out] M-major, b=X [T][in] N-major
+ * ------------------------------------------------------------------------- */
+odc_status odc_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, int64_t lda,
+                         int64_t ldb, int64_t ldd, int a_mn_major, int b_mn_major, int d_dtype, int accumulate,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
  * Load balancer (host C++, bit-exact restatement).  src/partition.cpp
  * strategy: 0 local-sort, 1 lb-micro, 2 lb-mini, 3 verl-native, 4 verl-optimized
  * ------------------------------------------------------------------------- */

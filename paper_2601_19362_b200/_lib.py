@@ -72,6 +72,7 @@ SIGNATURES = {
     "odc_ctx_epoch": (C.c_int64, [vp]),
     "odc_copy_segments": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), i64p, C.c_int, vp]),
     "odc_l2_flush": (C.c_int, [vp, i64, vp]),
+    "odc_gemm_bf16": (C.c_int, [vp, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "odc_plan_json": (C.c_int, [C.c_int, i64p, i64, C.c_int, C.c_int, i64, C.c_double, C.c_double, C.c_int,
                                 C.c_uint64, C.c_char_p, i64, i64p]),
     "odc_plan_flat": (C.c_int, [C.c_int, i64p, i64, C.c_int, C.c_int, i64, C.c_double, C.c_double, C.c_uint64,

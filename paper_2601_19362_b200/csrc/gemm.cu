@@ -1,0 +1,364 @@
+// gemm.cu — bf16 GEMM on the 5th-generation tensor cores (tcgen05) for the
+// worker's dense layers (fwd X·Wᵀ, dgrad dY·W, wgrad dYᵀ·X). No reference
+// counterpart (the reference only has the cost model, src/cost_model.cpp:14-18).
+//
+//   D[M,N] (+)= A·Bᵀ,  A: [M][K] (K-major) or [K][M] (M-major)
+//                      B: [N][K] (K-major) or [K][N] (N-major)
+//
+// Structure (one 128 x BN output tile per CTA, warp-specialised):
+//   warp 0       TMA producer: 2D tensor-map loads (128B swizzle) of the A/B
+//                k-slices into a kStages-deep smem ring (mbarrier full/empty)
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
+//                (kind::f16, M=128, N=BN, K=16 per instruction, fp32 accum in
+//                TMEM); tcgen05.commit releases smem stages / signals epilogue
+//   warps 2..5   epilogue: tcgen05.ld 32x32b TMEM -> registers -> bf16/fp32
+//                vector stores (each warp owns its TMEM lane quadrant)
+// Operand majorness is handled entirely by the UMMA smem descriptors and the
+// TMA boxes (K-major: box {64 K, rows}; MN-major: boxes {64 MN, 64 K}), so no
+// operand is ever transposed in memory.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace odc {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack
+    static constexpr int kTmemCols = BN;                         // fp32 accumulator columns
+};
+
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, unsigned long long* bar, void* smem, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(smem)),
+        "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm100 version bits = 1
+__device__ __forceinline__ std::uint64_t smem_desc(unsigned addr, unsigned lbo, unsigned sbo) {
+    std::uint64_t d = 0;
+    d |= static_cast<std::uint64_t>((addr & 0x3FFFF) >> 4);
+    d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // version
+    d |= 2ull << 61;  // layout: SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: bf16 x bf16 -> f32, M=128, N=BN
+__host__ __device__ constexpr unsigned instr_desc(int bn, int a_mn_major, int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(a_mn_major) << 15) |
+           (static_cast<unsigned>(b_mn_major) << 16) | (static_cast<unsigned>(bn >> 3) << 17) |
+           (static_cast<unsigned>(BM >> 4) << 24);
+}
+
+struct Args {
+    void* D;
+    long long M, N, K, ldd;
+    int d_f32, accumulate;
+    int a_mn, b_mn;  // 1 = MN-major operand
+    int tiles_m, tiles_n;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Args g) {
+    using C = Cfg<BN>;
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) unsigned long long full_bar[C::kStages], empty_bar[C::kStages], tmem_full;
+    __shared__ unsigned tmem_base;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // grouped rasterisation: 8 M-tiles share the same N-tiles for L2 reuse
+    const int tile = blockIdx.x;
+    const int group = 8;
+    const int per_group = group * g.tiles_n;
+    const int gid = tile / per_group, first_m = gid * group;
+    const int gsize = min(group, g.tiles_m - first_m);
+    const int tm = first_m + (tile % per_group) % gsize;
+    const int tn = (tile % per_group) / gsize;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int k_tiles = static_cast<int>((g.K + BK - 1) / BK);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_init(&tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
+                     "n"(C::kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            for (int kt = 0; kt < k_tiles; ++kt) {
+                const int s = kt % C::kStages;
+                if (kt >= C::kStages) mbar_wait(&empty_bar[s], ((kt / C::kStages) - 1) & 1);
+                char* sa = smem + s * C::kStageBytes;
+                char* sb = sa + C::kABytes;
+                mbar_expect_tx(&full_bar[s], C::kStageBytes);
+                const int k0 = kt * BK;
+                if (!g.a_mn) {
+                    tma_load_2d(&map_a, &full_bar[s], sa, k0, m0);
+                } else {
+                    tma_load_2d(&map_a, &full_bar[s], sa, m0, k0);
+                    tma_load_2d(&map_a, &full_bar[s], sa + 64 * BK * 2, m0 + 64, k0);
+                }
+                if (!g.b_mn) {
+                    tma_load_2d(&map_b, &full_bar[s], sb, k0, n0);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BN / 64; ++j) tma_load_2d(&map_b, &full_bar[s], sb + j * 64 * BK * 2, n0 + 64 * j, k0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const unsigned idesc = instr_desc(BN, g.a_mn, g.b_mn);
+            // K-major: rows of 128 B, 8-row atoms 1024 B apart (SBO), k-step +32 B
+            // MN-major: 64-element MN runs, 8-k-row atoms 1024 B apart (SBO),
+            //           next 64 MN at LBO = BK*128 B, k-step +2048 B
+            const unsigned a_lbo = g.a_mn ? BK * 128 : 16, b_lbo = g.b_mn ? BK * 128 : 16;
+            const unsigned a_step = g.a_mn ? 2048 : 32, b_step = g.b_mn ? 2048 : 32;
+            for (int kt = 0; kt < k_tiles; ++kt) {
+                const int s = kt % C::kStages;
+                mbar_wait(&full_bar[s], (kt / C::kStages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned sa = su32(smem + s * C::kStageBytes);
+                const unsigned sb = sa + C::kABytes;
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk) {
+                    const std::uint64_t da = smem_desc(sa + kk * a_step, a_lbo, 1024);
+                    const std::uint64_t db = smem_desc(sb + kk * b_step, b_lbo, 1024);
+                    const unsigned acc = (kt > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem),
+                        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                        : "memory");
+                }
+                // frees the smem stage once these MMAs have read it
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 su32(&empty_bar[s]))
+                             : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             su32(&tmem_full))
+                         : "memory");
+        }
+    } else {  // ---- epilogue warps 2..5
+        mbar_wait(&tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int quad = warp % 4;  // TMEM lane quadrant this warp may access
+        const long long row = m0 + quad * 32 + lane;
+        const bool row_ok = row < g.M;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            unsigned r[32];
+            const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(c);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (!row_ok) continue;
+            const long long col0 = n0 + c;
+            if (col0 >= g.N) continue;
+            const bool full = col0 + 32 <= g.N;
+            if (g.d_f32) {
+                float* out = static_cast<float*>(g.D) + row * g.ldd + col0;
+                if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                               __uint_as_float(r[j + 3]));
+                        if (g.accumulate) {
+                            const float4 o = *reinterpret_cast<const float4*>(out + j);
+                            v.x += o.x;
+                            v.y += o.y;
+                            v.z += o.z;
+                            v.w += o.w;
+                        }
+                        *reinterpret_cast<float4*>(out + j) = v;
+                    }
+                } else {
+                    for (int j = 0; j < 32 && col0 + j < g.N; ++j)
+                        out[j] = __uint_as_float(r[j]) + (g.accumulate ? out[j] : 0.f);
+                }
+            } else {
+                __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + col0;
+                if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        uint4 v;
+                        unsigned* w = reinterpret_cast<unsigned*>(&v);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            float lo = __uint_as_float(r[j + 2 * q]), hi = __uint_as_float(r[j + 2 * q + 1]);
+                            if (g.accumulate) {
+                                lo += __bfloat162float(out[j + 2 * q]);
+                                hi += __bfloat162float(out[j + 2 * q + 1]);
+                            }
+                            __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+                            w[q] = *reinterpret_cast<unsigned*>(&h);
+                        }
+                        *reinterpret_cast<uint4*>(out + j) = v;
+                    }
+                } else {
+                    for (int j = 0; j < 32 && col0 + j < g.N; ++j) {
+                        float x = __uint_as_float(r[j]) + (g.accumulate ? __bfloat162float(out[j]) : 0.f);
+                        out[j] = __float2bfloat16_rn(x);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ host
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D bf16 tensor map: inner dim (contiguous) x outer dim, row pitch in elements
+CUtensorMap make_map(const void* base, long long inner, long long outer, long long pitch, int box_inner, int box_outer) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw odcsim::ParamError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+template <int BN>
+cudaError_t launch(const void* A, const void* B, const Args& g, long long lda, long long ldb, cudaStream_t s) {
+    using C = Cfg<BN>;
+    static thread_local int configured = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured != dev) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return e;
+        configured = dev;
+    }
+    // A: K-major [M][K] (box 64 x 128) or M-major [K][M] (box 64 x 64)
+    CUtensorMap ma = g.a_mn ? make_map(A, g.M, g.K, lda, 64, BK) : make_map(A, g.K, g.M, lda, BK, BM);
+    CUtensorMap mb = g.b_mn ? make_map(B, g.N, g.K, ldb, 64, BK) : make_map(B, g.K, g.N, ldb, BK, BN);
+    count_launch();
+    gemm_kernel<BN><<<g.tiles_m * g.tiles_n, kThreads, C::kSmem, s>>>(ma, mb, g);
+    return cudaGetLastError();
+}
+
+}  // namespace gemm
+}  // namespace odc
+
+extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, std::int64_t M, std::int64_t N,
+                                    std::int64_t K, std::int64_t lda, std::int64_t ldb, std::int64_t ldd, int a_mn_major,
+                                    int b_mn_major, int d_dtype, int accumulate, void* stream) {
+    return odc::guard([&] {
+        using odcsim::ParamError;
+        if (M < 1 || N < 1 || K < 1) throw ParamError("gemm dims must be >= 1");
+        if (d_dtype != ODC_BF16 && d_dtype != ODC_F32) throw ParamError("gemm output must be bf16 or f32");
+        if ((lda * 2) % 16 || (ldb * 2) % 16) throw ParamError("gemm operand pitches must be multiples of 8 elements");
+        if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(B) % 16)
+            throw ParamError("gemm operands must be 16-byte aligned");
+        odc::gemm::Args g{};
+        g.D = D;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.ldd = ldd;
+        g.d_f32 = d_dtype == ODC_F32;
+        g.accumulate = accumulate;
+        g.a_mn = a_mn_major ? 1 : 0;
+        g.b_mn = b_mn_major ? 1 : 0;
+        g.tiles_m = static_cast<int>((M + odc::gemm::BM - 1) / odc::gemm::BM);
+        cudaError_t e;
+        if (N <= 128) {
+            g.tiles_n = static_cast<int>((N + 127) / 128);
+            e = odc::gemm::launch<128>(A, B, g, lda, ldb, reinterpret_cast<cudaStream_t>(stream));
+        } else {
+            g.tiles_n = static_cast<int>((N + 255) / 256);
+            e = odc::gemm::launch<256>(A, B, g, lda, ldb, reinterpret_cast<cudaStream_t>(stream));
+        }
+        if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
+    });
+}

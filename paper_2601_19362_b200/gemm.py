@@ -1,0 +1,48 @@
+"""Python entry to the tcgen05 bf16 GEMM of libodc.so (csrc/gemm.cu).
+
+    linear_fwd(x, w)      y  = x · wᵀ          x [T, in], w [out, in]
+    linear_dgrad(dy, w)   dx = dy · w          dy [T, out]
+    linear_wgrad(dy, x)   dw = dyᵀ · x  (fp32) -> [out, in]
+Operands are used in place (MN-major smem descriptors), never transposed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def gemm(a, b, out, M, N, K, lda, ldb, a_mn, b_mn, accumulate=False, stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    dt = _lib.ODC_F32 if out.dtype == torch.float32 else _lib.ODC_BF16
+    check(lib().odc_gemm_bf16(_p(a), _p(b), _p(out), M, N, K, lda, ldb, out.stride(0), int(a_mn), int(b_mn), dt,
+                              int(accumulate), C.c_void_p(s.cuda_stream)))
+    return out
+
+
+def linear_fwd(x, w, out=None):
+    T, K = x.shape
+    N = w.shape[0]
+    out = torch.empty(T, N, dtype=torch.bfloat16, device=x.device) if out is None else out
+    return gemm(x, w, out, T, N, K, x.stride(0), w.stride(0), 0, 0)
+
+
+def linear_dgrad(dy, w, out=None):
+    T, N_out = dy.shape
+    K_in = w.shape[1]
+    out = torch.empty(T, K_in, dtype=torch.bfloat16, device=dy.device) if out is None else out
+    return gemm(dy, w, out, T, K_in, N_out, dy.stride(0), w.stride(0), 0, 1)
+
+
+def linear_wgrad(dy, x, out=None, accumulate=False):
+    T, N_out = dy.shape
+    K_in = x.shape[1]
+    out = torch.empty(N_out, K_in, dtype=torch.float32, device=dy.device) if out is None else out
+    return gemm(dy, x, out, N_out, K_in, T, dy.stride(0), x.stride(0), 1, 1, accumulate=accumulate)

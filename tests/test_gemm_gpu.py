@@ -1,0 +1,36 @@
+"""tcgen05 GEMM parity vs torch fp32 matmul of the same bf16 operands.
+Tolerance: bf16 outputs within bf16 rounding (rtol 1e-2 / atol 1e-2 on unit-
+scale data); fp32 outputs (wgrad) within rtol 2e-3 of the fp32 reference
+(accumulation order differs)."""
+import pytest
+import torch
+
+from paper_2601_19362_b200 import gemm as G
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _r(*s):
+    return (torch.randn(*s, device=DEV) * 0.5).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("T,inn,out", [(128, 64, 128), (1000, 1536, 256), (4096, 1536, 8960), (333, 8960, 1536),
+                                       (257, 192, 320)])
+def test_fwd_dgrad_wgrad(T, inn, out):
+    x, w, dy = _r(T, inn), _r(out, inn), _r(T, out)
+    y = G.linear_fwd(x, w)
+    torch.testing.assert_close(y.float(), x.float() @ w.float().t(), rtol=1e-2, atol=2e-2 * (inn / 64) ** 0.5)
+    dx = G.linear_dgrad(dy, w)
+    torch.testing.assert_close(dx.float(), dy.float() @ w.float(), rtol=1e-2, atol=2e-2 * (out / 64) ** 0.5)
+    dw = G.linear_wgrad(dy, x)
+    ref = dy.float().t() @ x.float()
+    torch.testing.assert_close(dw, ref, rtol=2e-3, atol=2e-3 * (T / 64) ** 0.5)
+
+
+def test_accumulate_f32():
+    x, dy = _r(512, 256), _r(512, 384)
+    acc = torch.randn(384, 256, device=DEV)
+    want = acc + dy.float().t() @ x.float()
+    G.linear_wgrad(dy, x, out=acc, accumulate=True)
+    torch.testing.assert_close(acc, want, rtol=2e-3, atol=2e-2)
