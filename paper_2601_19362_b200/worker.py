@@ -1,0 +1,416 @@
+"""SFT worker: the caller of the ODC path (SURVEY §3 target call stack).
+
+One rank = one GPU. For every microbatch of this rank's queue (LB-Mini plan for
+ODC, LB-Micro for the FSDP comparison), a Qwen2.5/Llama-shaped decoder runs a
+packed-varlen forward and a hand-written backward:
+
+  forward   fetch unit l+1 on the comm stream while layer l computes
+  backward  fetch unit l-1 while layer l computes; push unit l's fp32
+            gradient as soon as its wgrads are done
+  minibatch end: comm.minibatch_end() then comm.adam()
+
+Dense layers are tcgen05 GEMMs (csrc/gemm.cu, operands used in place);
+attention is flash-attn varlen (library, sm_100 build); the elementwise
+glue (RMSNorm, RoPE, SwiGLU, CE) is torch for now. Activations are kept for
+the backward (no recompute; they fit 180 GB for the 1.5B shape at 32K).
+
+Comm backends share one interface:
+  OdcComm   odc fetch / push / device barrier / fused AdamW (libodc.so)
+  FsdpComm  NCCL all_gather_into_tensor / reduce_scatter_tensor per unit
+            per microbatch (the comparison path), same AdamW kernel
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import gemm as G
+from .shapes import Shape
+
+try:  # library attention kernels (flash-attn 2.8, sm_100 cubins)
+    from flash_attn.flash_attn_interface import _flash_attn_varlen_backward, _flash_attn_varlen_forward
+except Exception:  # pragma: no cover - resolved at use
+    _flash_attn_varlen_forward = _flash_attn_varlen_backward = None
+
+ROPE_THETA = 1_000_000.0
+EPS = 1e-6
+
+
+# ----------------------------------------------------------------- layouts
+def layer_layout(s: Shape) -> List[Tuple[str, Tuple[int, ...]]]:
+    """Flat FSDP-unit layout of one decoder layer (element order in the unit)."""
+    qkv = s.d + 2 * s.kv_heads * s.head_dim
+    lay = [("qkv_w", (qkv, s.d))]
+    if s.qkv_bias:
+        lay.append(("qkv_b", (qkv,)))
+    lay += [("o_w", (s.d, s.d)), ("gu_w", (2 * s.ffn, s.d)), ("down_w", (s.d, s.ffn)), ("ln1", (s.d,)),
+            ("ln2", (s.d,))]
+    return lay
+
+
+def embed_layout(s: Shape) -> List[Tuple[str, Tuple[int, ...]]]:
+    lay = [("emb", (s.vocab, s.d)), ("norm", (s.d,))]
+    if not s.tied:
+        lay.append(("head", (s.vocab, s.d)))
+    return lay
+
+
+def numel(lay) -> int:
+    return sum(math.prod(sh) for _, sh in lay)
+
+
+def views(flat: torch.Tensor, lay) -> Dict[str, torch.Tensor]:
+    out, off = {}, 0
+    for name, sh in lay:
+        n = math.prod(sh)
+        out[name] = flat[off:off + n].view(*sh)
+        off += n
+    return out
+
+
+def unit_sizes(s: Shape) -> List[int]:
+    """FSDP units: 0 = embedding (+ final norm, + untied head), 1..L = layers."""
+    return [numel(embed_layout(s))] + [numel(layer_layout(s))] * s.layers
+
+
+def init_unit(s: Shape, unit: int, gen: torch.Generator, device) -> torch.Tensor:
+    lay = embed_layout(s) if unit == 0 else layer_layout(s)
+    flat = torch.empty(numel(lay), device=device)
+    v = views(flat, lay)
+    for name, t in v.items():
+        if name in ("ln1", "ln2", "norm"):
+            t.fill_(1.0)
+        elif name.endswith("_b"):
+            t.zero_()
+        else:
+            t.normal_(0.0, 0.02, generator=gen)
+    return flat
+
+
+# ------------------------------------------------------------ elementwise
+def rmsnorm_fwd(x, w):
+    xf = x.float()
+    rstd = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + EPS)
+    return (xf * rstd * w.float()).to(torch.bfloat16), rstd
+
+
+def rmsnorm_bwd(dy, x, w, rstd):
+    xhat = x.float() * rstd
+    dyf = dy.float()
+    dw = (dyf * xhat).sum(0)
+    dxhat = dyf * w.float()
+    dx = rstd * (dxhat - xhat * (dxhat * xhat).mean(-1, keepdim=True))
+    return dx, dw
+
+
+def rope_tables(positions: torch.Tensor, head_dim: int):
+    inv = 1.0 / (ROPE_THETA ** (torch.arange(0, head_dim, 2, device=positions.device, dtype=torch.float32) / head_dim))
+    ang = positions.float()[:, None] * inv[None, :]
+    return torch.cos(ang), torch.sin(ang)  # [T, hd/2]
+
+
+def rope_apply(x, cos, sin, inverse=False):
+    """x [T, H, hd] (rotate-half convention); inverse=True applies the transpose."""
+    h = x.shape[-1] // 2
+    x1, x2 = x[..., :h].float(), x[..., h:].float()
+    c, s = cos[:, None, :], sin[:, None, :]
+    if inverse:
+        s = -s
+    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1).to(torch.bfloat16)
+
+
+# ------------------------------------------------------------------ comm
+class OdcComm:
+    """ODC: point-to-point fetch/push over CUDA-IPC-mapped peer HBM."""
+
+    name = "odc"
+
+    def __init__(self, engine):
+        self.eng = engine
+
+    def fetch(self, unit, out, stream):
+        self.eng.fetch(unit, out, stream=stream)
+
+    def push(self, unit, grad, weight, stream):
+        self.eng.push(unit, grad, weight, stream=stream)
+
+    def minibatch_end(self, stream):
+        self.eng.minibatch_end(stream=stream)
+
+    def adam(self, stream, **kw):
+        self.eng.adam_step(stream=stream, **kw)
+
+
+class FsdpComm:
+    """FSDP comparison path: per-unit NCCL collectives every microbatch.
+    Owned shards live in the same engine arena (world=1 engine per rank
+    holding this rank's 1/N slice of every unit), AdamW is the same kernel."""
+
+    name = "fsdp"
+
+    def __init__(self, sizes: Sequence[int], rank: int, world: int, device, group=None):
+        import torch.distributed as dist
+
+        from .engine import OdcEngine
+
+        self.dist, self.group, self.rank, self.world = dist, group, rank, world
+        for n in sizes:
+            if n % world:
+                raise ValueError("FSDP path needs unit sizes divisible by the world size")
+        self.shard = [n // world for n in sizes]
+        self.local = OdcEngine(self.shard, rank=0, world=1, device=device)  # owned shards + AdamW state
+        self.bf = [torch.empty(n, dtype=torch.bfloat16, device=device) for n in self.shard]
+        self.rs = [torch.empty(n, dtype=torch.float32, device=device) for n in self.shard]
+        self.dirty = True
+
+    def set_params(self, unit, full_fp32):
+        sh = self.shard[unit]
+        self.local.set_params(unit, full_fp32[self.rank * sh:(self.rank + 1) * sh].contiguous())
+
+    def _refresh(self, stream):
+        if self.dirty:
+            for u in range(len(self.shard)):
+                self.local.fetch(u, self.bf[u], stream=stream)
+            self.dirty = False
+
+    def fetch(self, unit, out, stream):
+        with torch.cuda.stream(stream):
+            self._refresh(stream)
+            self.dist.all_gather_into_tensor(out, self.bf[unit], group=self.group)
+
+    def push(self, unit, grad, weight, stream):
+        with torch.cuda.stream(stream):
+            if weight != 1.0:  # per-rank token weight applied before the sum
+                grad.mul_(weight)
+            self.dist.reduce_scatter_tensor(self.rs[unit], grad, group=self.group)
+            self.local.push(unit, self.rs[unit], 1.0, stream=stream)
+
+    def minibatch_end(self, stream):
+        self.local.minibatch_end(stream=stream)
+
+    def adam(self, stream, **kw):
+        self.local.adam_step(stream=stream, **kw)
+        self.dirty = True
+
+
+# --------------------------------------------------------------- worker
+@dataclass
+class Batch:
+    ids: torch.Tensor        # [T] int64
+    labels: torch.Tensor     # [T] int64, -100 = ignore
+    positions: torch.Tensor  # [T]
+    cu_seqlens: torch.Tensor  # [n+1] int32
+    max_len: int
+    tokens: int
+
+
+def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, device) -> Batch:
+    """Synthetic packed microbatch: token ids seeded by the global sample id, so
+    every implementation sees identical data."""
+    ids, labels, pos, cu = [], [], [], [0]
+    for sid in sample_ids:
+        n = int(lens[sid])
+        g = torch.Generator().manual_seed(1_000_003 * (sid + 1))
+        t = torch.randint(0, vocab, (n,), generator=g)
+        ids.append(t)
+        lab = torch.full((n,), -100, dtype=torch.int64)
+        lab[:-1] = t[1:]
+        labels.append(lab)
+        pos.append(torch.arange(n))
+        cu.append(cu[-1] + n)
+    T = cu[-1]
+    return Batch(torch.cat(ids).to(device, non_blocking=True), torch.cat(labels).to(device, non_blocking=True),
+                 torch.cat(pos).to(device, non_blocking=True),
+                 torch.tensor(cu, dtype=torch.int32).to(device, non_blocking=True),
+                 max(int(lens[s]) for s in sample_ids), T)
+
+
+class Worker:
+    def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192):
+        if _flash_attn_varlen_forward is None:
+            raise ImportError("flash-attn (sm_100) is required for the worker's attention")
+        self.s, self.comm, self.dev = shape, comm, torch.device(device)
+        self.sizes = unit_sizes(shape)
+        self.L = shape.layers
+        self.ce_chunk = ce_chunk
+        self.comm_stream = torch.cuda.Stream(device=self.dev)
+        lsz = self.sizes[1]
+        self.pbuf = [torch.empty(lsz, dtype=torch.bfloat16, device=self.dev) for _ in range(2)]
+        self.gbuf = [torch.empty(lsz, dtype=torch.float32, device=self.dev) for _ in range(2)]
+        self.ebuf = torch.empty(self.sizes[0], dtype=torch.bfloat16, device=self.dev)
+        self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
+        self.busy_ms: List[float] = []
+
+    # --- stream helpers
+    def _fetch(self, unit, buf, after: Optional[torch.cuda.Event] = None):
+        if after is not None:
+            self.comm_stream.wait_event(after)
+        self.comm.fetch(unit, buf, self.comm_stream)
+        ev = torch.cuda.Event()
+        ev.record(self.comm_stream)
+        return ev
+
+    def microbatch(self, b: Batch, weight: float) -> torch.Tensor:
+        s, L = self.s, self.L
+        cur = torch.cuda.current_stream(self.dev)
+        hd, H, KV = s.head_dim, s.heads, s.kv_heads
+        T = b.tokens
+        scale = 1.0 / math.sqrt(hd)
+        cos, sin = rope_tables(b.positions, hd)
+        lay = layer_layout(s)
+
+        # ---------------- forward
+        ev_e = self._fetch(0, self.ebuf, after=_record(cur))
+        ev = self._fetch(1, self.pbuf[1 % 2], after=_record(cur))
+        cur.wait_event(ev_e)
+        E = views(self.ebuf, embed_layout(s))
+        h = E["emb"].index_select(0, b.ids)
+        saved = []
+        for l in range(1, L + 1):
+            cur.wait_event(ev)
+            P = views(self.pbuf[l % 2], lay)
+            if l < L:  # prefetch next unit into the other buffer once layer l-1's compute released it
+                ev = self._fetch(l + 1, self.pbuf[(l + 1) % 2], after=_record(cur))
+            x = h
+            a, r1 = rmsnorm_fwd(x, P["ln1"])
+            qkv = G.linear_fwd(a, P["qkv_w"])
+            if "qkv_b" in P:
+                qkv += P["qkv_b"]
+            q = qkv[:, :H * hd].view(T, H, hd)
+            k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
+            v = qkv[:, (H + KV) * hd:].view(T, KV, hd).contiguous()
+            q = rope_apply(q, cos, sin)
+            k = rope_apply(k, cos, sin)
+            o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len, 0.0,
+                                                      scale, True)
+            o2 = o.view(T, H * hd)
+            h = x + G.linear_fwd(o2, P["o_w"])
+            bn, r2 = rmsnorm_fwd(h, P["ln2"])
+            gu = G.linear_fwd(bn, P["gu_w"])
+            g_, u_ = gu[:, :s.ffn], gu[:, s.ffn:]
+            m = (torch.nn.functional.silu(g_.float()) * u_.float()).to(torch.bfloat16)
+            h2 = h + G.linear_fwd(m, P["down_w"])
+            saved.append((x, a, r1, q, k, v, o, lse, h, bn, r2, gu, m))
+            h = h2
+
+        # ---------------- LM head + CE (chunked), backward of the head in place
+        hf, rf = rmsnorm_fwd(h, E["norm"])
+        head = E["emb"] if s.tied else E["head"]
+        EG = views(self.egrad, embed_layout(s))
+        self.egrad.zero_()
+        dhf = torch.empty_like(hf)
+        n_valid = max(1, T - (b.cu_seqlens.numel() - 1))
+        loss = torch.zeros((), device=self.dev, dtype=torch.float32)
+        headg = EG["emb"] if s.tied else EG["head"]
+        for c0 in range(0, T, self.ce_chunk):
+            c1 = min(T, c0 + self.ce_chunk)
+            logits = G.linear_fwd(hf[c0:c1], head)
+            lf = logits.float()
+            lab = b.labels[c0:c1]
+            valid = lab >= 0
+            lse_c = torch.logsumexp(lf, -1)
+            tgt = lf.gather(1, lab.clamp(min=0)[:, None])[:, 0]
+            loss += ((lse_c - tgt) * valid).sum()
+            p = torch.softmax(lf, -1)
+            p.scatter_add_(1, lab.clamp(min=0)[:, None], -valid.float()[:, None])
+            p *= (valid.float() / n_valid)[:, None]
+            dl = p.to(torch.bfloat16)
+            del lf, p, logits
+            G.linear_dgrad(dl, head, out=dhf[c0:c1])
+            G.linear_wgrad(dl, hf[c0:c1], out=headg, accumulate=True)
+        loss /= n_valid
+        dh, dnorm = rmsnorm_bwd(dhf, h, E["norm"], rf)
+        EG["norm"].copy_(dnorm)
+        dh = dh.to(torch.bfloat16)
+
+        # ---------------- backward through the layers
+        ev = self._fetch(L, self.pbuf[L % 2], after=_record(cur))
+        push_ev = [None, None]
+        for l in range(L, 0, -1):
+            cur.wait_event(ev)
+            P = views(self.pbuf[l % 2], lay)
+            if l > 1:
+                ev = self._fetch(l - 1, self.pbuf[(l - 1) % 2], after=_record(cur))
+            gi = l % 2
+            if push_ev[gi] is not None:  # grad buffer free once its previous push finished
+                cur.wait_event(push_ev[gi])
+            Gv = views(self.gbuf[gi], lay)
+            x, a, r1, q, k, v, o, lse, hmid, bn, r2, gu, m = saved[l - 1]
+            # MLP block
+            dm = G.linear_dgrad(dh, P["down_w"])
+            G.linear_wgrad(dh, m, out=Gv["down_w"])
+            g_, u_ = gu[:, :s.ffn].float(), gu[:, s.ffn:].float()
+            sg = torch.sigmoid(g_)
+            dmf = dm.float()
+            dgu = torch.cat([dmf * u_ * sg * (1 + g_ * (1 - sg)), dmf * g_ * sg], -1).to(torch.bfloat16)
+            dbn = G.linear_dgrad(dgu, P["gu_w"])
+            G.linear_wgrad(dgu, bn, out=Gv["gu_w"])
+            dx2, dln2 = rmsnorm_bwd(dbn, hmid, P["ln2"], r2)
+            Gv["ln2"].copy_(dln2)
+            dhm = (dh.float() + dx2).to(torch.bfloat16)
+            # attention block
+            do = G.linear_dgrad(dhm, P["o_w"])
+            G.linear_wgrad(dhm, o.view(T, -1), out=Gv["o_w"])
+            dq = torch.empty_like(q)
+            dk = torch.empty_like(k)
+            dv = torch.empty_like(v)
+            _flash_attn_varlen_backward(do.view(T, s.heads, hd), q, k, v, o, lse, dq, dk, dv, b.cu_seqlens,
+                                        b.cu_seqlens, b.max_len, b.max_len, 0.0, scale, True, -1, -1, 0.0, None,
+                                        False)
+            dq = rope_apply(dq, cos, sin, inverse=True)
+            dk = rope_apply(dk, cos, sin, inverse=True)
+            dqkv = torch.cat([dq.view(T, -1), dk.view(T, -1), dv.view(T, -1)], -1)
+            if "qkv_b" in P:
+                Gv["qkv_b"].copy_(dqkv.float().sum(0))
+            da = G.linear_dgrad(dqkv, P["qkv_w"])
+            G.linear_wgrad(dqkv, a, out=Gv["qkv_w"])
+            dx1, dln1 = rmsnorm_bwd(da, x, P["ln1"], r1)
+            Gv["ln1"].copy_(dln1)
+            dh = (dhm.float() + dx1).to(torch.bfloat16)
+            # push this unit's gradient as soon as it is complete
+            self.comm_stream.wait_event(_record(cur))
+            self.comm.push(l, self.gbuf[gi], weight, self.comm_stream)
+            push_ev[gi] = _record(self.comm_stream)
+            saved[l - 1] = None
+        # embedding: scatter-add of dh into the looked-up rows (+ tied head grad above)
+        EG["emb"].index_add_(0, b.ids, dh.float())
+        self.comm_stream.wait_event(_record(cur))
+        self.comm.push(0, self.egrad, weight, self.comm_stream)
+        cur.wait_event(_record(self.comm_stream))
+        return loss
+
+    def empty_microbatch(self):
+        """FSDP padding microbatch (src/partition.cpp:305-307, :339): joins every
+        collective in exactly the order microbatch() issues them, computes nothing."""
+        cur = torch.cuda.current_stream(self.dev)
+        L = self.L
+        self._fetch(0, self.ebuf, after=_record(cur))
+        for u in range(1, L + 1):
+            self._fetch(u, self.pbuf[u % 2])
+        self._fetch(L, self.pbuf[L % 2])
+        self.egrad.zero_()
+        for g in self.gbuf:
+            g.zero_()
+        self.comm_stream.wait_event(_record(cur))
+        for l in range(L, 0, -1):
+            if l > 1:
+                self._fetch(l - 1, self.pbuf[(l - 1) % 2])
+            self.comm.push(l, self.gbuf[l % 2], 0.0, self.comm_stream)
+        self.comm.push(0, self.egrad, 0.0, self.comm_stream)
+        cur.wait_event(_record(self.comm_stream))
+
+    def minibatch_end(self, lr=1e-5):
+        cur = torch.cuda.current_stream(self.dev)
+        self.comm_stream.wait_event(_record(cur))
+        self.comm.minibatch_end(self.comm_stream)
+        self.comm.adam(self.comm_stream, lr=lr)
+        cur.wait_event(_record(self.comm_stream))
+
+
+def _record(stream) -> torch.cuda.Event:
+    e = torch.cuda.Event()
+    e.record(stream)
+    return e
