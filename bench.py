@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="odc", choices=["odc", "reference"])
-    ap.add_argument("--workload", default="odc_minibatch_comm", choices=["odc_minibatch_comm"])
+    ap.add_argument("--workload", default="sft", choices=["sft", "odc_minibatch_comm"])
+    ap.add_argument("--no-fsdp", action="store_true", help="skip the same-box NCCL FSDP comparison arm")
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--push-mode", default="red", choices=["red", "slot"])
     ap.add_argument("--minibs", type=int, default=8)
@@ -175,6 +176,27 @@ def run_reference(args):
         return
     shape = SHAPES[args.model]
     world = args.gpus
+    if args.workload == "sft":
+        from paper_2601_19362_b200 import partition as P
+        from paper_2601_19362_b200 import worker as W
+
+        lens = workload_lengths()
+        plan = P.plan_flat("lb-mini", lens, world, args.minibs, 32768, P.CostModel(1.0, shape.beta_over_alpha(), 1))
+        sizes = W.unit_sizes(shape)
+        for k in range(args.warmup):
+            cpu_tokens_baseline(lens, plan, [k], sizes, world)
+        t0 = time.perf_counter()
+        vals = [cpu_tokens_baseline(lens, plan, [args.warmup + k], sizes, world) for k in range(args.steps)]
+        wall = time.perf_counter() - t0
+        tps = sum(v["value"] for v in vals) / len(vals)
+        line = {"metric": METRIC, "impl": "reference", "value": round(tps, 2), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "odc_sft", "model": shape.name, "world": world},
+                "cpu_baseline": {**vals[0], "value": round(tps, 2)},
+                "e2e": {"value": round(tps, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     for _ in range(args.warmup):
         cpu_reference_sample(world, shape.layer_elems, 1)
     secs, byts = 0.0, 0
@@ -192,10 +214,226 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def analytic(lens, plan_odc, plan_fsdp, beta, steps):
+    """Compute-only prediction of the reference's evaluator (src/runtime.cpp:
+    52-79) on the same plans: ODC total = max_d busy, collective total = sum over
+    microbatch slots of max_d; cost alpha*s^2 + beta*s per sample."""
+    def c(mb):
+        return sum(float(lens[i]) ** 2 + beta * lens[i] for i in mb)
+
+    odc = coll = 0.0
+    for k in steps:
+        odc += max(sum(c(mb) for mb in dev) for dev in plan_odc[k % len(plan_odc)])
+        fs = plan_fsdp[k % len(plan_fsdp)]
+        coll += sum(max(c(dev[m]) if dev[m] else 0.0 for dev in fs) for m in range(len(fs[0])))
+    return coll / odc if odc else None
+
+
+def run_sft(args):
+    """Workload "sft" (default): one ODC optimizer step of Qwen2.5-1.5B-shaped
+    SFT on the long-tail workload per bench step (see module docstring)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_19362_b200 import _lib
+    from paper_2601_19362_b200 import gemm as G
+    from paper_2601_19362_b200 import partition as P
+    from paper_2601_19362_b200 import worker as W
+    from paper_2601_19362_b200.engine import OdcEngine
+    from paper_2601_19362_b200.shapes import SHAPES
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    shape = SHAPES[args.model]
+    sizes = W.unit_sizes(shape)
+    lens = workload_lengths()
+    beta = shape.beta_over_alpha()
+    cost = P.CostModel(1.0, beta, 1)
+    plan_odc = P.plan_flat("lb-mini", lens, world, args.minibs, 32768, cost)
+    plan_fsdp = P.plan_flat("lb-micro", lens, world, args.minibs, 32768, cost)
+    do_fsdp = world > 1 and not args.no_fsdp
+
+    eng = OdcEngine(sizes, rank=rank, world=world, device=local, push_mode=args.push_mode,
+                    fetch_ctas=args.fetch_ctas, push_ctas=args.push_ctas)
+    fsdp = W.FsdpComm(sizes, rank, world, dev) if do_fsdp else None
+    gen = torch.Generator(device=dev).manual_seed(0)
+    for u in range(len(sizes)):  # identical full units on every rank, each keeps its slice
+        full = W.init_unit(shape, u, gen, dev)
+        eng.set_params(u, full)
+        if fsdp:
+            fsdp.set_params(u, full)
+        del full
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    warm_steps = list(range(args.warmup))
+    timed_steps = list(range(args.warmup, args.warmup + args.steps))
+
+    def step_tokens(plan, k):
+        return sum(lens[i] for dv in plan[k % len(plan)] for mb in dv for i in mb)
+
+    def run_arm(comm, plan, resident: bool, record=False, clocks=None):
+        worker = W.Worker(shape, comm, dev)
+        stream = torch.cuda.current_stream()
+
+        def one(k, batches=None):
+            mine = plan[k % len(plan)][rank]
+            total = float(step_tokens(plan, k))
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t2 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            loss = torch.zeros((), device=dev)
+            for j, mb in enumerate(mine):
+                if not mb:
+                    worker.empty_microbatch()
+                    continue
+                b = batches[j] if batches is not None else W.make_batch(lens, mb, shape.vocab, dev)
+                ntok = sum(lens[i] for i in mb)
+                loss += worker.microbatch(b, ntok / total) * (ntok / total)
+            t1.record(stream)
+            worker.minibatch_end()
+            t2.record(stream)
+            return t0, t1, t2, loss
+
+        for k in warm_steps:
+            one(k)
+        torch.cuda.synchronize()
+        eng.check()
+        pre = {}
+        if resident:
+            for k in timed_steps:
+                pre[k] = [W.make_batch(lens, mb, shape.vocab, dev) if mb else None
+                          for mb in plan[k % len(plan)][rank]]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        G.recorder = G.Recorder() if record else None
+        n0 = _lib.kernel_launches()
+        evs, losses = [], []
+        a = torch.cuda.Event(enable_timing=True)
+        z = torch.cuda.Event(enable_timing=True)
+        ctx = clocks if clocks is not None else _Null()
+        with ctx:  # nvidia-smi clock/throttle sampling covers exactly the timed steps
+            a.record(stream)
+            for k in timed_steps:
+                t0, t1, t2, loss = one(k, pre.get(k))
+                evs.append((t0, t1, t2))
+                if not resident:
+                    losses.append(loss.item())  # D2H of the step's result (e2e)
+            z.record(stream)
+            torch.cuda.synchronize()
+        launches = _lib.kernel_launches() - n0
+        eng.check()
+        gsum = G.recorder.summary() if record else None
+        G.recorder = None
+        ms = a.elapsed_time(z)
+        busy = sum(e0.elapsed_time(e1) for e0, e1, _ in evs)
+        t = torch.tensor([ms, busy, float(launches)], device=dev, dtype=torch.float64)
+        if world > 1:
+            allb = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allb, t)
+            allb = torch.stack(allb).cpu()
+        else:
+            allb = t[None].cpu()
+        ms_max = allb[:, 0].max().item()
+        idle = 1.0 - allb[:, 1].sum().item() / (world * ms_max)
+        del worker
+        torch.cuda.empty_cache()
+        toks = sum(step_tokens(plan, k) for k in timed_steps)
+        return {"ms": ms_max, "tokens": toks, "tps": toks / (ms_max / 1e3), "idle": idle,
+                "launches": int(allb[:, 2].sum().item()), "gemm": gsum,
+                "loss": (sum(losses) / len(losses)) if losses else None}
+
+    clk = ClockSampler(local)
+    res = run_arm(W.OdcComm(eng), plan_odc, resident=True, record=True, clocks=clk)
+    e2e = run_arm(W.OdcComm(eng), plan_odc, resident=False) if not args.no_e2e else None
+    fs = run_arm(fsdp, plan_fsdp, resident=True) if do_fsdp else None
+
+    hbm, hbm_kind = peaks()
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        tflops_peak, tkind = float(pk["bf16_tflops_sustained"]), "measured sustained"
+    except Exception:
+        tflops_peak, tkind = 1400.0, "fallback sustained"
+    roof = None
+    if res["gemm"]:
+        gm = res["gemm"]
+        ach = gm["flops"] / (gm["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": tflops_peak, "unit": "TFLOP/s",
+                "peak_kind": tkind, "frac": round(ach / tflops_peak, 4), "kernel": "odc::gemm::gemm_kernel (tcgen05)",
+                "launches": gm["launches"], "ms_per_launch": round(gm["ms"] / gm["launches"], 4),
+                "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": None}
+    h2d = sum(16 * lens[i] + 8 for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_tokens_baseline(lens, plan_odc, timed_steps, sizes, world)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(res["tps"], 1), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"] / args.steps, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (random-init weights, seeded random token ids of the workload lengths)",
+                "config": {"workload": "odc_sft", "model": shape.name, "plan": "lb-mini (odc) / lb-micro (fsdp)",
+                           "minibs_per_rank": args.minibs, "budget_tokens": 32768,
+                           "lengths": "lognormal(8,1.5) n=2048 cap=32768 seed=0, floor 512",
+                           "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
+                           "tokens_timed": res["tokens"], "l2": "inputs > L2 (GBs of activations/units), no flush"},
+                "idle_fraction": round(res["idle"], 4),
+                "vs_fsdp": ({"fsdp_tokens_per_s": round(fs["tps"], 1), "speedup": round(res["tps"] / fs["tps"], 4),
+                             "fsdp_idle_fraction": round(fs["idle"], 4),
+                             "analytic_compute_only_speedup": round(analytic(lens, plan_odc, plan_fsdp, beta,
+                                                                             timed_steps), 4)}
+                            if fs else None),
+                "roofline": roof, "clocks": clk.summary(),
+                "e2e": ({"value": round(e2e["tps"], 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / args.steps),
+                         "d2h_bytes_per_step": 4, "loss": e2e["loss"],
+                         "note": "token ids/labels/positions built on host per microbatch, copied H2D inside the "
+                                 "timed region; loss read back D2H every step"} if e2e else None),
+                "cpu_baseline": cpu, "gpu_launches": res["launches"]}
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def cpu_tokens_baseline(lens, plan, steps, sizes, world):
+    """Reference CPU path of one step, extrapolated from a bounded sample: the
+    reference fabric (ShardFabric<float>) moving one FSDP layer unit for one
+    microbatch (2 gathers + 1 scatter_accumulate per client + finalize), times
+    units x microbatches of the step, plus the reference plan() time."""
+    from oracle import refbind as R
+
+    s, _, kind, sample = cpu_reference_sample(world, sizes[1], 1)
+    micro = sum(len(dv) for k in steps for dv in plan[k % len(plan)])
+    t_plan = R.plan_seconds("lb-mini", lens, world, 8, 32768, 1.0, 30467.0, 1) if R.available() else 0.0
+    t = s * len(sizes) * micro / max(1, world) + t_plan * len(steps)
+    toks = sum(lens[i] for k in steps for dv in plan[k % len(plan)] for mb in dv for i in mb)
+    return {"value": round(toks / t, 2), "unit": "tokens/s", "cores": 1, "kind": kind,
+            "sample": sample + f"; extrapolated x{len(sizes)} units x {micro} microbatches + plan()"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "sft":
+        return run_sft(args)
 
     import torch
     import torch.distributed as dist

@@ -19,11 +19,37 @@ def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
+class Recorder:
+    """Optional live timing of every GEMM launch (CUDA events on the launching
+    stream) for the bench's roofline: records (flops, start, end)."""
+
+    def __init__(self):
+        self.rows = []
+
+    def summary(self):
+        if not self.rows:
+            return None
+        ms = [s.elapsed_time(e) for _, s, e in self.rows]
+        fl = sum(f for f, _, _ in self.rows)
+        return {"launches": len(self.rows), "flops": fl, "ms": sum(ms)}
+
+
+recorder = None
+
+
 def gemm(a, b, out, M, N, K, lda, ldb, a_mn, b_mn, accumulate=False, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     dt = _lib.ODC_F32 if out.dtype == torch.float32 else _lib.ODC_BF16
+    rec = recorder
+    if rec is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
     check(lib().odc_gemm_bf16(_p(a), _p(b), _p(out), M, N, K, lda, ldb, out.stride(0), int(a_mn), int(b_mn), dt,
                               int(accumulate), C.c_void_p(s.cuda_stream)))
+    if rec is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(s)
+        rec.rows.append((2.0 * M * N * K, e0, e1))
     return out
 
 
