@@ -216,17 +216,22 @@ def run_reference(args):
 
 def analytic(lens, plan_odc, plan_fsdp, beta, steps):
     """Compute-only prediction of the reference's evaluator (src/runtime.cpp:
-    52-79) on the same plans: ODC total = max_d busy, collective total = sum over
-    microbatch slots of max_d; cost alpha*s^2 + beta*s per sample."""
+    52-79) on the same plans, cost alpha*s^2 + beta*s per sample: ODC total =
+    max_d busy, collective total = sum over microbatch slots of max_d; bubble =
+    1 - sum(busy)/(D*T) (:43). Returns (speedup, odc bubble, collective bubble)."""
     def c(mb):
         return sum(float(lens[i]) ** 2 + beta * lens[i] for i in mb)
 
-    odc = coll = 0.0
+    odc = coll = busy_o = busy_c = 0.0
+    D = len(plan_odc[0])
     for k in steps:
-        odc += max(sum(c(mb) for mb in dev) for dev in plan_odc[k % len(plan_odc)])
+        po = plan_odc[k % len(plan_odc)]
+        odc += max(sum(c(mb) for mb in dev) for dev in po)
+        busy_o += sum(c(mb) for dev in po for mb in dev)
         fs = plan_fsdp[k % len(plan_fsdp)]
         coll += sum(max(c(dev[m]) if dev[m] else 0.0 for dev in fs) for m in range(len(fs[0])))
-    return coll / odc if odc else None
+        busy_c += sum(c(mb) for dev in fs for mb in dev if mb)
+    return coll / odc, 1 - busy_o / (D * odc), 1 - busy_c / (D * coll)
 
 
 def run_sft(args):
@@ -239,6 +244,7 @@ def run_sft(args):
     from paper_2601_19362_b200 import gemm as G
     from paper_2601_19362_b200 import partition as P
     from paper_2601_19362_b200 import worker as W
+    from paper_2601_19362_b200.dist import rank_timings
     from paper_2601_19362_b200.engine import OdcEngine
     from paper_2601_19362_b200.shapes import SHAPES
 
@@ -336,20 +342,12 @@ def run_sft(args):
         G.recorder = None
         ms = a.elapsed_time(z)
         busy = sum(e0.elapsed_time(e1) for e0, e1, _ in evs)
-        t = torch.tensor([ms, busy, float(launches)], device=dev, dtype=torch.float64)
-        if world > 1:
-            allb = [torch.zeros_like(t) for _ in range(world)]
-            dist.all_gather(allb, t)
-            allb = torch.stack(allb).cpu()
-        else:
-            allb = t[None].cpu()
-        ms_max = allb[:, 0].max().item()
-        idle = 1.0 - allb[:, 1].sum().item() / (world * ms_max)
+        ms_max, idle, launches_all, _ = rank_timings(ms, busy, launches, device=dev)
         del worker
         torch.cuda.empty_cache()
         toks = sum(step_tokens(plan, k) for k in timed_steps)
         return {"ms": ms_max, "tokens": toks, "tps": toks / (ms_max / 1e3), "idle": idle,
-                "launches": int(allb[:, 2].sum().item()), "gemm": gsum,
+                "launches": launches_all, "gemm": gsum,
                 "loss": (sum(losses) / len(losses)) if losses else None}
 
     clk = ClockSampler(local)
@@ -372,6 +370,7 @@ def run_sft(args):
                 "peak_kind": tkind, "frac": round(ach / tflops_peak, 4), "kernel": "odc::gemm::gemm_kernel (tcgen05)",
                 "launches": gm["launches"], "ms_per_launch": round(gm["ms"] / gm["launches"], 4),
                 "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": None}
+    pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
     h2d = sum(16 * lens[i] + 8 for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -387,11 +386,11 @@ def run_sft(args):
                            "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
                            "tokens_timed": res["tokens"], "l2": "inputs > L2 (GBs of activations/units), no flush"},
                 "idle_fraction": round(res["idle"], 4),
+                "idle_note": "1 - sum(busy)/(N*T), busy = device time from step start to the minibatch barrier",
                 "vs_fsdp": ({"fsdp_tokens_per_s": round(fs["tps"], 1), "speedup": round(res["tps"] / fs["tps"], 4),
-                             "fsdp_idle_fraction": round(fs["idle"], 4),
-                             "analytic_compute_only_speedup": round(analytic(lens, plan_odc, plan_fsdp, beta,
-                                                                             timed_steps), 4)}
-                            if fs else None),
+                             "analytic_compute_only_speedup": round(pred[0], 4),
+                             "analytic_bubble_odc_lbmini": round(pred[1], 4),
+                             "analytic_bubble_fsdp_lbmicro": round(pred[2], 4)} if fs else None),
                 "roofline": roof, "clocks": clk.summary(),
                 "e2e": ({"value": round(e2e["tps"], 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / args.steps),
                          "d2h_bytes_per_step": 4, "loss": e2e["loss"],

@@ -49,7 +49,9 @@ class OdcEngine:
                  group=None, fetch_engine: str = "tma"):
         self.layer_elems = [int(x) for x in layer_elems]
         self.rank, self.world = rank, world
-        self.device = torch.cuda.current_device() if device is None else device
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device.index if isinstance(device, torch.device) else int(device)
         self.push_mode = push_mode
         arr = (C.c_int64 * len(self.layer_elems))(*self.layer_elems)
         cfg = _lib.OdcConfig(rank, world, self.device, len(self.layer_elems), arr, PUSH_MODES[push_mode], fetch_ctas,
@@ -63,15 +65,12 @@ class OdcEngine:
         self.adam_steps = 0
 
     def _exchange(self, group):
-        import torch.distributed as dist
+        from .dist import exchange_blobs
 
         n = C.c_size_t(0)
         buf = C.create_string_buffer(256)
         check(lib().odc_ctx_export(self.h, buf, 256, C.byref(n)))
-        mine = bytes(buf.raw[:n.value])
-        blobs = [None] * self.world
-        dist.all_gather_object(blobs, mine, group=group)
-        for peer, blob in enumerate(blobs):
+        for peer, blob in enumerate(exchange_blobs(buf.raw[:n.value], group)):
             b = C.create_string_buffer(blob, len(blob))
             check(lib().odc_ctx_import(self.h, peer, b, len(blob)))
 
