@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ODC_ABI_VERSION 2
+#define ODC_ABI_VERSION 3
 
 typedef enum {
     ODC_OK = 0,
@@ -191,14 +191,39 @@ odc_status odc_l2_flush(void* scratch, int64_t bytes, void* stream);
  *   D[M,N] (+)= A · B^T with fp32 accumulation in TMEM
  *   A stored [M][K] (a_mn_major = 0) or [K][M] (a_mn_major = 1), pitch lda
  *   B stored [N][K] (b_mn_major = 0) or [K][N] (b_mn_major = 1), pitch ldb
- *   D row-major [M][ldd], d_dtype ODC_BF16 or ODC_F32; accumulate: D += A·B^T
+ *   D row-major [M][ldd], d_dtype ODC_BF16 or ODC_F32; accumulate: D += A·B^T;
+ *   C (optional, bf16 output only): D = A·B^T + C, C with D's shape and ldd (fused residual)
  * fwd  X·W^T : a=X [T][in] K-major,  b=W [out][in] K-major
  * dgrad dY·W : a=dY [T][out] K-major, b=W [out][in] N-major
  * wgrad dY^T·X: a=dY [T][out] M-major, b=X [T][in] N-major
  * ------------------------------------------------------------------------- */
-odc_status odc_gemm_bf16(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, int64_t lda,
-                         int64_t ldb, int64_t ldd, int a_mn_major, int b_mn_major, int d_dtype, int accumulate,
-                         void* stream);
+odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, int64_t M, int64_t N, int64_t K,
+                         int64_t lda, int64_t ldb, int64_t ldd, int a_mn_major, int b_mn_major, int d_dtype,
+                         int accumulate, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Fused elementwise kernels of the SFT worker (csrc/worker_kernels.cu).
+ * bf16 tensors row-major and 16-byte aligned; fp32 for rstd / dw / loss.
+ * ------------------------------------------------------------------------- */
+odc_status odc_w_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t T, int d, float eps,
+                             void* stream);
+/* out = resid (optional) + dx; dw += sum over rows of dy * x * rstd */
+odc_status odc_w_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* resid,
+                             void* out, float* dw, int64_t T, int d, void* stream);
+/* packed qkv [T][(H+2KV)hd] (+bias) -> q [T][H][hd], k, v [T][KV][hd], RoPE on q,k;
+ * table = float2 {cos, sin} [max_pos][hd/2] */
+odc_status odc_w_qkv_rope_fwd(const void* qkv, const void* bias, const void* table, const int64_t* pos, void* q,
+                              void* k, void* v, int64_t T, int H, int KV, int hd, void* stream);
+odc_status odc_w_qkv_rope_bwd(const void* dq, const void* dk, const void* dv, const void* table, const int64_t* pos,
+                              void* dqkv, int64_t T, int H, int KV, int hd, void* stream);
+/* out[j] += sum_t m[t][j] (fp32) */
+odc_status odc_w_col_sum(const void* m, float* out, int64_t T, int n, void* stream);
+odc_status odc_w_swiglu_fwd(const void* gu, void* m, int64_t T, int ffn, void* stream);
+odc_status odc_w_swiglu_bwd(const void* dm, const void* gu, void* dgu, int64_t T, int ffn, void* stream);
+/* logits [rows][vocab] bf16 overwritten by (softmax - onehot) * scale (0 for label < 0);
+ * *loss += sum over labelled rows of (logsumexp - logit[label]) */
+odc_status odc_w_ce_fwd_bwd(void* logits, const int64_t* labels, int64_t rows, int64_t vocab, float scale,
+                            float* loss, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Load balancer (host C++, bit-exact restatement).  src/partition.cpp

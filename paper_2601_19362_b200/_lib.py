@@ -72,7 +72,16 @@ SIGNATURES = {
     "odc_ctx_epoch": (C.c_int64, [vp]),
     "odc_copy_segments": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), i64p, C.c_int, vp]),
     "odc_l2_flush": (C.c_int, [vp, i64, vp]),
-    "odc_gemm_bf16": (C.c_int, [vp, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+    "odc_gemm_bf16": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                vp]),
+    "odc_w_rmsnorm_fwd": (C.c_int, [vp, vp, vp, vp, i64, C.c_int, C.c_float, vp]),
+    "odc_w_rmsnorm_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, vp]),
+    "odc_w_qkv_rope_fwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, vp]),
+    "odc_w_qkv_rope_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, vp]),
+    "odc_w_col_sum": (C.c_int, [vp, vp, i64, C.c_int, vp]),
+    "odc_w_swiglu_fwd": (C.c_int, [vp, vp, i64, C.c_int, vp]),
+    "odc_w_swiglu_bwd": (C.c_int, [vp, vp, vp, i64, C.c_int, vp]),
+    "odc_w_ce_fwd_bwd": (C.c_int, [vp, vp, i64, i64, C.c_float, vp, vp]),
     "odc_plan_json": (C.c_int, [C.c_int, i64p, i64, C.c_int, C.c_int, i64, C.c_double, C.c_double, C.c_int,
                                 C.c_uint64, C.c_char_p, i64, i64p]),
     "odc_plan_flat": (C.c_int, [C.c_int, i64p, i64, C.c_int, C.c_int, i64, C.c_double, C.c_double, C.c_uint64,
@@ -97,7 +106,7 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.odc_abi_version() != 2:
+        if L.odc_abi_version() != 3:
             raise ImportError("libodc.so ABI version mismatch")
         _lib = L
     return _lib

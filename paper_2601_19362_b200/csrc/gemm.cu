@@ -88,6 +88,7 @@ __host__ __device__ constexpr unsigned instr_desc(int bn, int a_mn_major, int b_
 
 struct Args {
     void* D;
+    const void* C;  // optional bf16 residual: D = A·Bᵀ + C (same shape / ldd as D)
     long long M, N, K, ldd;
     int d_f32, accumulate;
     int a_mn, b_mn;  // 1 = MN-major operand
@@ -239,18 +240,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             } else {
                 __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + col0;
+                const __nv_bfloat16* add = g.C ? static_cast<const __nv_bfloat16*>(g.C) + row * g.ldd + col0
+                                               : (g.accumulate ? out : nullptr);
                 if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 8) {
-                        uint4 v;
+                        uint4 v, a4 = make_uint4(0, 0, 0, 0);
+                        if (add) a4 = *reinterpret_cast<const uint4*>(add + j);
+                        const unsigned* aw = reinterpret_cast<const unsigned*>(&a4);
                         unsigned* w = reinterpret_cast<unsigned*>(&v);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            float lo = __uint_as_float(r[j + 2 * q]), hi = __uint_as_float(r[j + 2 * q + 1]);
-                            if (g.accumulate) {
-                                lo += __bfloat162float(out[j + 2 * q]);
-                                hi += __bfloat162float(out[j + 2 * q + 1]);
-                            }
+                            const float lo = __uint_as_float(r[j + 2 * q]) + __uint_as_float(aw[q] << 16);
+                            const float hi = __uint_as_float(r[j + 2 * q + 1]) + __uint_as_float(aw[q] & 0xffff0000u);
                             __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
                             w[q] = *reinterpret_cast<unsigned*>(&h);
                         }
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 } else {
                     for (int j = 0; j < 32 && col0 + j < g.N; ++j) {
-                        float x = __uint_as_float(r[j]) + (g.accumulate ? __bfloat162float(out[j]) : 0.f);
+                        float x = __uint_as_float(r[j]) + (add ? __bfloat162float(add[j]) : 0.f);
                         out[j] = __float2bfloat16_rn(x);
                     }
                 }
@@ -330,9 +332,9 @@ cudaError_t launch(const void* A, const void* B, const Args& g, long long lda, l
 }  // namespace gemm
 }  // namespace odc
 
-extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, std::int64_t M, std::int64_t N,
-                                    std::int64_t K, std::int64_t lda, std::int64_t ldb, std::int64_t ldd, int a_mn_major,
-                                    int b_mn_major, int d_dtype, int accumulate, void* stream) {
+extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, std::int64_t M,
+                                    std::int64_t N, std::int64_t K, std::int64_t lda, std::int64_t ldb, std::int64_t ldd,
+                                    int a_mn_major, int b_mn_major, int d_dtype, int accumulate, void* stream) {
     return odc::guard([&] {
         using odcsim::ParamError;
         if (M < 1 || N < 1 || K < 1) throw ParamError("gemm dims must be >= 1");
@@ -341,7 +343,9 @@ extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, std::
         if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(B) % 16)
             throw ParamError("gemm operands must be 16-byte aligned");
         odc::gemm::Args g{};
+        if (C && d_dtype != ODC_BF16) throw ParamError("gemm residual C requires a bf16 output");
         g.D = D;
+        g.C = C;
         g.M = M;
         g.N = N;
         g.K = K;

@@ -1,0 +1,81 @@
+"""ctypes wrappers of the worker's fused sm_100a elementwise kernels
+(csrc/worker_kernels.cu). bf16 activations, fp32 statistics/gradients."""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import check, lib
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _s():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def rmsnorm_fwd(x, w, eps=1e-6):
+    T, d = x.shape
+    y = torch.empty_like(x)
+    rstd = torch.empty(T, dtype=torch.float32, device=x.device)
+    check(lib().odc_w_rmsnorm_fwd(_p(x), _p(w), _p(y), _p(rstd), T, d, eps, _s()))
+    return y, rstd
+
+
+def rmsnorm_bwd(dy, x, w, rstd, dw_accum, resid=None):
+    """returns resid + dx (bf16); dw_accum (fp32 [d]) += sum_rows dy * xhat."""
+    T, d = x.shape
+    out = torch.empty_like(x)
+    check(lib().odc_w_rmsnorm_bwd(_p(dy), _p(x), _p(w), _p(rstd), _p(resid), _p(out), _p(dw_accum), T, d, _s()))
+    return out
+
+
+def rope_table(max_pos, head_dim, theta, device):
+    inv = 1.0 / (theta ** (torch.arange(0, head_dim, 2, dtype=torch.float64) / head_dim))
+    ang = torch.arange(max_pos, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.stack([torch.cos(ang), torch.sin(ang)], -1).float().contiguous().to(device)  # [P, hd/2, 2]
+
+
+def qkv_rope_fwd(qkv, bias, table, pos, H, KV, hd):
+    T = qkv.shape[0]
+    q = torch.empty(T, H, hd, dtype=torch.bfloat16, device=qkv.device)
+    k = torch.empty(T, KV, hd, dtype=torch.bfloat16, device=qkv.device)
+    v = torch.empty(T, KV, hd, dtype=torch.bfloat16, device=qkv.device)
+    check(lib().odc_w_qkv_rope_fwd(_p(qkv), _p(bias), _p(table), _p(pos), _p(q), _p(k), _p(v), T, H, KV, hd, _s()))
+    return q, k, v
+
+
+def qkv_rope_bwd(dq, dk, dv, table, pos, H, KV, hd):
+    T = dq.shape[0]
+    out = torch.empty(T, (H + 2 * KV) * hd, dtype=torch.bfloat16, device=dq.device)
+    check(lib().odc_w_qkv_rope_bwd(_p(dq), _p(dk), _p(dv), _p(table), _p(pos), _p(out), T, H, KV, hd, _s()))
+    return out
+
+
+def col_sum_(m, out):
+    T, n = m.shape
+    check(lib().odc_w_col_sum(_p(m), _p(out), T, n, _s()))
+    return out
+
+
+def swiglu_fwd(gu, ffn):
+    T = gu.shape[0]
+    m = torch.empty(T, ffn, dtype=torch.bfloat16, device=gu.device)
+    check(lib().odc_w_swiglu_fwd(_p(gu), _p(m), T, ffn, _s()))
+    return m
+
+
+def swiglu_bwd(dm, gu, ffn):
+    T = gu.shape[0]
+    dgu = torch.empty_like(gu)
+    check(lib().odc_w_swiglu_bwd(_p(dm), _p(gu), _p(dgu), T, ffn, _s()))
+    return dgu
+
+
+def ce_fwd_bwd_(logits, labels, scale, loss_accum):
+    rows, V = logits.shape
+    check(lib().odc_w_ce_fwd_bwd(_p(logits), _p(labels), rows, V, float(scale), _p(loss_accum), _s()))
+    return logits

@@ -37,15 +37,17 @@ class Recorder:
 recorder = None
 
 
-def gemm(a, b, out, M, N, K, lda, ldb, a_mn, b_mn, accumulate=False, stream=None):
+def gemm(a, b, out, M, N, K, lda, ldb, a_mn, b_mn, accumulate=False, stream=None, residual=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     dt = _lib.ODC_F32 if out.dtype == torch.float32 else _lib.ODC_BF16
     rec = recorder
     if rec is not None:
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(s)
-    check(lib().odc_gemm_bf16(_p(a), _p(b), _p(out), M, N, K, lda, ldb, out.stride(0), int(a_mn), int(b_mn), dt,
-                              int(accumulate), C.c_void_p(s.cuda_stream)))
+    if residual is not None:
+        assert residual.dtype == torch.bfloat16 and residual.stride(0) == out.stride(0)
+    check(lib().odc_gemm_bf16(_p(a), _p(b), _p(out), None if residual is None else _p(residual), M, N, K, lda, ldb,
+                              out.stride(0), int(a_mn), int(b_mn), dt, int(accumulate), C.c_void_p(s.cuda_stream)))
     if rec is not None:
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(s)
@@ -53,11 +55,12 @@ def gemm(a, b, out, M, N, K, lda, ldb, a_mn, b_mn, accumulate=False, stream=None
     return out
 
 
-def linear_fwd(x, w, out=None):
+def linear_fwd(x, w, out=None, residual=None):
+    """y = x·wᵀ (+ residual, fused in the epilogue)."""
     T, K = x.shape
     N = w.shape[0]
     out = torch.empty(T, N, dtype=torch.bfloat16, device=x.device) if out is None else out
-    return gemm(x, w, out, T, N, K, x.stride(0), w.stride(0), 0, 0)
+    return gemm(x, w, out, T, N, K, x.stride(0), w.stride(0), 0, 0, residual=residual)
 
 
 def linear_dgrad(dy, w, out=None):

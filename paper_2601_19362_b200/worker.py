@@ -11,8 +11,10 @@ packed-varlen forward and a hand-written backward:
 
 Dense layers are tcgen05 GEMMs (csrc/gemm.cu, operands used in place);
 attention is flash-attn varlen (library, sm_100 build); the elementwise
-glue (RMSNorm, RoPE, SwiGLU, CE) is torch for now. Activations are kept for
-the backward (no recompute; they fit 180 GB for the 1.5B shape at 32K).
+glue (RMSNorm, bias+RoPE+split, SwiGLU, CE) is fused sm_100a kernels
+(csrc/worker_kernels.cu) and residual adds ride in the GEMM epilogue.
+Activations are kept for the backward (no recompute; they fit 180 GB for the
+1.5B shape at 32K tokens).
 
 Comm backends share one interface:
   OdcComm   odc fetch / push / device barrier / fused AdamW (libodc.so)
@@ -27,6 +29,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import torch
 
+from . import fused as F
 from . import gemm as G
 from .shapes import Shape
 
@@ -90,36 +93,11 @@ def init_unit(s: Shape, unit: int, gen: torch.Generator, device) -> torch.Tensor
     return flat
 
 
-# ------------------------------------------------------------ elementwise
-def rmsnorm_fwd(x, w):
-    xf = x.float()
-    rstd = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + EPS)
-    return (xf * rstd * w.float()).to(torch.bfloat16), rstd
-
-
-def rmsnorm_bwd(dy, x, w, rstd):
-    xhat = x.float() * rstd
-    dyf = dy.float()
-    dw = (dyf * xhat).sum(0)
-    dxhat = dyf * w.float()
-    dx = rstd * (dxhat - xhat * (dxhat * xhat).mean(-1, keepdim=True))
-    return dx, dw
-
-
+# ------------------------------------------------------------ rope (test reference)
 def rope_tables(positions: torch.Tensor, head_dim: int):
     inv = 1.0 / (ROPE_THETA ** (torch.arange(0, head_dim, 2, device=positions.device, dtype=torch.float32) / head_dim))
     ang = positions.float()[:, None] * inv[None, :]
     return torch.cos(ang), torch.sin(ang)  # [T, hd/2]
-
-
-def rope_apply(x, cos, sin, inverse=False):
-    """x [T, H, hd] (rotate-half convention); inverse=True applies the transpose."""
-    h = x.shape[-1] // 2
-    x1, x2 = x[..., :h].float(), x[..., h:].float()
-    c, s = cos[:, None, :], sin[:, None, :]
-    if inverse:
-        s = -s
-    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1).to(torch.bfloat16)
 
 
 # ------------------------------------------------------------------ comm
@@ -229,7 +207,7 @@ def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, devic
 
 
 class Worker:
-    def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192):
+    def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192, max_positions: int = 65536):
         if _flash_attn_varlen_forward is None:
             raise ImportError("flash-attn (sm_100) is required for the worker's attention")
         self.s, self.comm, self.dev = shape, comm, torch.device(device)
@@ -242,7 +220,7 @@ class Worker:
         self.gbuf = [torch.empty(lsz, dtype=torch.float32, device=self.dev) for _ in range(2)]
         self.ebuf = torch.empty(self.sizes[0], dtype=torch.bfloat16, device=self.dev)
         self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
-        self.busy_ms: List[float] = []
+        self.rope = F.rope_table(max_positions, shape.head_dim, ROPE_THETA, self.dev)
 
     # --- stream helpers
     def _fetch(self, unit, buf, after: Optional[torch.cuda.Event] = None):
@@ -259,8 +237,8 @@ class Worker:
         hd, H, KV = s.head_dim, s.heads, s.kv_heads
         T = b.tokens
         scale = 1.0 / math.sqrt(hd)
-        cos, sin = rope_tables(b.positions, hd)
         lay = layer_layout(s)
+        tab = self.rope
 
         # ---------------- forward
         ev_e = self._fetch(0, self.ebuf, after=_record(cur))
@@ -272,59 +250,41 @@ class Worker:
         for l in range(1, L + 1):
             cur.wait_event(ev)
             P = views(self.pbuf[l % 2], lay)
-            if l < L:  # prefetch next unit into the other buffer once layer l-1's compute released it
+            if l < L:  # prefetch the next unit into the other buffer once layer l-1 released it
                 ev = self._fetch(l + 1, self.pbuf[(l + 1) % 2], after=_record(cur))
             x = h
-            a, r1 = rmsnorm_fwd(x, P["ln1"])
+            a, r1 = F.rmsnorm_fwd(x, P["ln1"])
             qkv = G.linear_fwd(a, P["qkv_w"])
-            if "qkv_b" in P:
-                qkv += P["qkv_b"]
-            q = qkv[:, :H * hd].view(T, H, hd)
-            k = qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd)
-            v = qkv[:, (H + KV) * hd:].view(T, KV, hd).contiguous()
-            q = rope_apply(q, cos, sin)
-            k = rope_apply(k, cos, sin)
+            q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), tab, b.positions, H, KV, hd)
+            del qkv
             o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len, 0.0,
                                                       scale, True)
-            o2 = o.view(T, H * hd)
-            h = x + G.linear_fwd(o2, P["o_w"])
-            bn, r2 = rmsnorm_fwd(h, P["ln2"])
+            hm = G.linear_fwd(o.view(T, H * hd), P["o_w"], residual=x)
+            bn, r2 = F.rmsnorm_fwd(hm, P["ln2"])
             gu = G.linear_fwd(bn, P["gu_w"])
-            g_, u_ = gu[:, :s.ffn], gu[:, s.ffn:]
-            m = (torch.nn.functional.silu(g_.float()) * u_.float()).to(torch.bfloat16)
-            h2 = h + G.linear_fwd(m, P["down_w"])
-            saved.append((x, a, r1, q, k, v, o, lse, h, bn, r2, gu, m))
-            h = h2
+            m = F.swiglu_fwd(gu, s.ffn)
+            h = G.linear_fwd(m, P["down_w"], residual=hm)
+            saved.append((x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m))
 
-        # ---------------- LM head + CE (chunked), backward of the head in place
-        hf, rf = rmsnorm_fwd(h, E["norm"])
+        # ---------------- final norm, LM head + CE (chunked); head backward in place
+        hf, rf = F.rmsnorm_fwd(h, E["norm"])
         head = E["emb"] if s.tied else E["head"]
-        EG = views(self.egrad, embed_layout(s))
         self.egrad.zero_()
+        EG = views(self.egrad, embed_layout(s))
+        headg = EG["emb"] if s.tied else EG["head"]
         dhf = torch.empty_like(hf)
         n_valid = max(1, T - (b.cu_seqlens.numel() - 1))
         loss = torch.zeros((), device=self.dev, dtype=torch.float32)
-        headg = EG["emb"] if s.tied else EG["head"]
         for c0 in range(0, T, self.ce_chunk):
             c1 = min(T, c0 + self.ce_chunk)
             logits = G.linear_fwd(hf[c0:c1], head)
-            lf = logits.float()
-            lab = b.labels[c0:c1]
-            valid = lab >= 0
-            lse_c = torch.logsumexp(lf, -1)
-            tgt = lf.gather(1, lab.clamp(min=0)[:, None])[:, 0]
-            loss += ((lse_c - tgt) * valid).sum()
-            p = torch.softmax(lf, -1)
-            p.scatter_add_(1, lab.clamp(min=0)[:, None], -valid.float()[:, None])
-            p *= (valid.float() / n_valid)[:, None]
-            dl = p.to(torch.bfloat16)
-            del lf, p, logits
+            dl = F.ce_fwd_bwd_(logits, b.labels[c0:c1], 1.0 / n_valid, loss)  # logits -> dlogits in place
             G.linear_dgrad(dl, head, out=dhf[c0:c1])
             G.linear_wgrad(dl, hf[c0:c1], out=headg, accumulate=True)
+            del logits, dl
         loss /= n_valid
-        dh, dnorm = rmsnorm_bwd(dhf, h, E["norm"], rf)
-        EG["norm"].copy_(dnorm)
-        dh = dh.to(torch.bfloat16)
+        dh = F.rmsnorm_bwd(dhf, h, E["norm"], rf, EG["norm"])
+        del dhf, hf
 
         # ---------------- backward through the layers
         ev = self._fetch(L, self.pbuf[L % 2], after=_record(cur))
@@ -338,38 +298,34 @@ class Worker:
             if push_ev[gi] is not None:  # grad buffer free once its previous push finished
                 cur.wait_event(push_ev[gi])
             Gv = views(self.gbuf[gi], lay)
-            x, a, r1, q, k, v, o, lse, hmid, bn, r2, gu, m = saved[l - 1]
+            for name in ("ln1", "ln2", "qkv_b"):  # atomically accumulated parts
+                if name in Gv:
+                    Gv[name].zero_()
+            x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = saved[l - 1]
             # MLP block
             dm = G.linear_dgrad(dh, P["down_w"])
             G.linear_wgrad(dh, m, out=Gv["down_w"])
-            g_, u_ = gu[:, :s.ffn].float(), gu[:, s.ffn:].float()
-            sg = torch.sigmoid(g_)
-            dmf = dm.float()
-            dgu = torch.cat([dmf * u_ * sg * (1 + g_ * (1 - sg)), dmf * g_ * sg], -1).to(torch.bfloat16)
+            dgu = F.swiglu_bwd(dm, gu, s.ffn)
+            del dm
             dbn = G.linear_dgrad(dgu, P["gu_w"])
             G.linear_wgrad(dgu, bn, out=Gv["gu_w"])
-            dx2, dln2 = rmsnorm_bwd(dbn, hmid, P["ln2"], r2)
-            Gv["ln2"].copy_(dln2)
-            dhm = (dh.float() + dx2).to(torch.bfloat16)
+            del dgu
+            dhm = F.rmsnorm_bwd(dbn, hm, P["ln2"], r2, Gv["ln2"], resid=dh)
             # attention block
             do = G.linear_dgrad(dhm, P["o_w"])
             G.linear_wgrad(dhm, o.view(T, -1), out=Gv["o_w"])
             dq = torch.empty_like(q)
             dk = torch.empty_like(k)
             dv = torch.empty_like(v)
-            _flash_attn_varlen_backward(do.view(T, s.heads, hd), q, k, v, o, lse, dq, dk, dv, b.cu_seqlens,
-                                        b.cu_seqlens, b.max_len, b.max_len, 0.0, scale, True, -1, -1, 0.0, None,
-                                        False)
-            dq = rope_apply(dq, cos, sin, inverse=True)
-            dk = rope_apply(dk, cos, sin, inverse=True)
-            dqkv = torch.cat([dq.view(T, -1), dk.view(T, -1), dv.view(T, -1)], -1)
-            if "qkv_b" in P:
-                Gv["qkv_b"].copy_(dqkv.float().sum(0))
+            _flash_attn_varlen_backward(do.view(T, H, hd), q, k, v, o, lse, dq, dk, dv, b.cu_seqlens, b.cu_seqlens,
+                                        b.max_len, b.max_len, 0.0, scale, True, -1, -1, 0.0, None, False)
+            dqkv = F.qkv_rope_bwd(dq, dk, dv, tab, b.positions, H, KV, hd)
+            del dq, dk, dv, do
+            if "qkv_b" in Gv:
+                F.col_sum_(dqkv, Gv["qkv_b"])
             da = G.linear_dgrad(dqkv, P["qkv_w"])
             G.linear_wgrad(dqkv, a, out=Gv["qkv_w"])
-            dx1, dln1 = rmsnorm_bwd(da, x, P["ln1"], r1)
-            Gv["ln1"].copy_(dln1)
-            dh = (dhm.float() + dx1).to(torch.bfloat16)
+            dh = F.rmsnorm_bwd(da, x, P["ln1"], r1, Gv["ln1"], resid=dhm)
             # push this unit's gradient as soon as it is complete
             self.comm_stream.wait_event(_record(cur))
             self.comm.push(l, self.gbuf[gi], weight, self.comm_stream)
