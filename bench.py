@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", default="odc", choices=["odc", "reference"])
     ap.add_argument("--workload", default="sft", choices=["sft", "odc_minibatch_comm"])
     ap.add_argument("--no-fsdp", action="store_true", help="skip the same-box NCCL FSDP comparison arm")
+    ap.add_argument("--trace", default="", help="write a Chrome trace (reference schema) of one extra ODC step")
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--push-mode", default="red", choices=["red", "slot"])
     ap.add_argument("--minibs", type=int, default=8)
@@ -355,6 +356,9 @@ def run_sft(args):
     e2e = run_arm(W.OdcComm(eng), plan_odc, resident=False) if not args.no_e2e else None
     fs = run_arm(fsdp, plan_fsdp, resident=True) if do_fsdp else None
 
+    if args.trace:
+        write_trace(args.trace, shape, W.OdcComm(eng), plan_odc, lens, timed_steps[0], rank, world, dev)
+
     hbm, hbm_kind = peaks()
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -401,6 +405,43 @@ def run_sft(args):
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def write_trace(path, shape, comm, plan, lens, k, rank, world, dev):
+    """One extra (untimed) ODC step with per-layer CUDA-event spans, gathered to
+    rank 0 and written in the reference's Chrome-trace schema."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_19362_b200 import worker as W
+
+    worker = W.Worker(shape, comm, dev)
+    worker.tracer = W.Tracer(rank)
+    cur = torch.cuda.current_stream()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    worker.tracer.start(cur)
+    total = float(sum(lens[i] for dv in plan[k % len(plan)] for mb in dv for i in mb))
+    for mb in plan[k % len(plan)][rank]:
+        ntok = sum(lens[i] for i in mb)
+        worker.microbatch(W.make_batch(lens, mb, shape.vocab, dev), ntok / total)
+    worker.tracer.span("barrier", 0, cur, False)
+    row = worker.tracer.rows[-1]
+    worker.minibatch_end()
+    W.Tracer.end(row, cur)
+    torch.cuda.synchronize()
+    evs = worker.tracer.events()
+    allv = [None] * world
+    if world > 1:
+        dist.all_gather_object(allv, evs)
+    else:
+        allv = [evs]
+    if rank == 0:
+        with open(path, "w") as f:
+            json.dump(W.chrome_trace(allv), f)
+    del worker
+    torch.cuda.empty_cache()
 
 
 class _Null:

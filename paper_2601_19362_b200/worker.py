@@ -174,6 +174,57 @@ class FsdpComm:
         self.dirty = True
 
 
+# ---------------------------------------------------------------- trace
+class Tracer:
+    """Measured timeline in the reference's Chrome-trace schema
+    (src/commsim.cpp:240-258: name "<kind> m<mb> l<layer>", cat compute|comm,
+    ph X, pid = rank, tid 0 compute / 1 comm, ts/dur in microseconds,
+    args.volume_elems for comm). Spans are CUDA events on the stream that ran
+    the work, so they show real overlap of fetch/push with compute."""
+
+    def __init__(self, rank: int):
+        self.rank, self.rows, self.t0 = rank, [], None
+        self.mb = 0
+
+    def start(self, stream):
+        self.t0 = torch.cuda.Event(enable_timing=True)
+        self.t0.record(stream)
+
+    def span(self, kind, layer, stream, is_comm, volume=0):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        row = [kind, self.mb, layer, is_comm, volume, e0, None]
+        self.rows.append(row)
+        return row
+
+    @staticmethod
+    def end(row, stream):
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        row[6] = e1
+
+    def events(self):
+        out = []
+        for kind, mb, layer, is_comm, vol, e0, e1 in self.rows:
+            if e1 is None:
+                continue
+            ts = self.t0.elapsed_time(e0) * 1e3
+            ev = {"name": f"{kind} m{mb} l{layer}", "cat": "comm" if is_comm else "compute", "ph": "X",
+                  "pid": self.rank, "tid": 1 if is_comm else 0, "ts": ts, "dur": e0.elapsed_time(e1) * 1e3}
+            if is_comm:
+                ev["args"] = {"volume_elems": vol}
+            out.append(ev)
+        return out
+
+    def busy_ms(self):
+        return sum(e0.elapsed_time(e1) for k, _, _, c, _, e0, e1 in self.rows if not c and e1 is not None)
+
+
+def chrome_trace(events_per_rank) -> dict:
+    evs = [e for evs in events_per_rank for e in evs]
+    return {"traceEvents": evs, "displayTimeUnit": "ms"}
+
+
 # --------------------------------------------------------------- worker
 @dataclass
 class Batch:
@@ -221,12 +272,16 @@ class Worker:
         self.ebuf = torch.empty(self.sizes[0], dtype=torch.bfloat16, device=self.dev)
         self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
         self.rope = F.rope_table(max_positions, shape.head_dim, ROPE_THETA, self.dev)
+        self.tracer: Optional[Tracer] = None
 
     # --- stream helpers
     def _fetch(self, unit, buf, after: Optional[torch.cuda.Event] = None):
         if after is not None:
             self.comm_stream.wait_event(after)
+        tr = self.tracer.span("gather", unit, self.comm_stream, True, buf.numel()) if self.tracer else None
         self.comm.fetch(unit, buf, self.comm_stream)
+        if tr:
+            Tracer.end(tr, self.comm_stream)
         ev = torch.cuda.Event()
         ev.record(self.comm_stream)
         return ev
@@ -253,6 +308,7 @@ class Worker:
             if l < L:  # prefetch the next unit into the other buffer once layer l-1 released it
                 ev = self._fetch(l + 1, self.pbuf[(l + 1) % 2], after=_record(cur))
             x = h
+            tr = self.tracer.span("fwd", l, cur, False) if self.tracer else None
             a, r1 = F.rmsnorm_fwd(x, P["ln1"])
             qkv = G.linear_fwd(a, P["qkv_w"])
             q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), tab, b.positions, H, KV, hd)
@@ -265,6 +321,8 @@ class Worker:
             m = F.swiglu_fwd(gu, s.ffn)
             h = G.linear_fwd(m, P["down_w"], residual=hm)
             saved.append((x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m))
+            if tr:
+                Tracer.end(tr, cur)
 
         # ---------------- final norm, LM head + CE (chunked); head backward in place
         hf, rf = F.rmsnorm_fwd(h, E["norm"])
@@ -302,6 +360,7 @@ class Worker:
                 if name in Gv:
                     Gv[name].zero_()
             x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = saved[l - 1]
+            tr = self.tracer.span("bwd", l, cur, False) if self.tracer else None
             # MLP block
             dm = G.linear_dgrad(dh, P["down_w"])
             G.linear_wgrad(dh, m, out=Gv["down_w"])
@@ -326,9 +385,14 @@ class Worker:
             da = G.linear_dgrad(dqkv, P["qkv_w"])
             G.linear_wgrad(dqkv, a, out=Gv["qkv_w"])
             dh = F.rmsnorm_bwd(da, x, P["ln1"], r1, Gv["ln1"], resid=dhm)
+            if tr:
+                Tracer.end(tr, cur)
             # push this unit's gradient as soon as it is complete
             self.comm_stream.wait_event(_record(cur))
+            trp = self.tracer.span("reduce", l, self.comm_stream, True, self.gbuf[gi].numel()) if self.tracer else None
             self.comm.push(l, self.gbuf[gi], weight, self.comm_stream)
+            if trp:
+                Tracer.end(trp, self.comm_stream)
             push_ev[gi] = _record(self.comm_stream)
             saved[l - 1] = None
         # embedding: scatter-add of dh into the looked-up rows (+ tied head grad above)
@@ -336,6 +400,8 @@ class Worker:
         self.comm_stream.wait_event(_record(cur))
         self.comm.push(0, self.egrad, weight, self.comm_stream)
         cur.wait_event(_record(self.comm_stream))
+        if self.tracer:
+            self.tracer.mb += 1
         return loss
 
     def empty_microbatch(self):

@@ -1,0 +1,48 @@
+"""Kernel-time breakdown of one SFT step at N=1 via torch.profiler (CUPTI
+activity tracing, no kernel replay): share of device time per kernel family."""
+import os
+import sys
+from collections import defaultdict
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2601_19362_b200 import partition as P  # noqa: E402
+from paper_2601_19362_b200 import worker as W  # noqa: E402
+from paper_2601_19362_b200.engine import OdcEngine  # noqa: E402
+from paper_2601_19362_b200.shapes import SHAPES  # noqa: E402
+
+shape = SHAPES[os.environ.get("MODEL", "qwen2.5-1.5b")]
+dev = torch.device("cuda", 0)
+sizes = W.unit_sizes(shape)
+lens = [max(512, x) for x in P.generate_synthetic(("lognormal", 8.0, 1.5), 2048, 32768, 0)]
+plan = P.plan_flat("lb-mini", lens, 1, 8, 32768, P.CostModel(1.0, shape.beta_over_alpha(), 1))
+eng = OdcEngine(sizes)
+gen = torch.Generator(device=dev).manual_seed(0)
+for u in range(len(sizes)):
+    eng.set_params(u, W.init_unit(shape, u, gen, dev))
+wk = W.Worker(shape, W.OdcComm(eng), dev)
+
+
+def step(k):
+    tot = float(sum(lens[i] for dv in plan[k] for mb in dv for i in mb))
+    for mb in plan[k][0]:
+        wk.microbatch(W.make_batch(lens, mb, shape.vocab, dev), sum(lens[i] for i in mb) / tot)
+    wk.minibatch_end()
+
+
+step(0)
+torch.cuda.synchronize()
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+    step(1)
+    torch.cuda.synchronize()
+agg = defaultdict(float)
+cnt = defaultdict(int)
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        agg[e.name[:80]] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+        cnt[e.name[:80]] += 1
+tot = sum(agg.values())
+print(f"total device time {tot / 1e3:.1f} ms; tokens {sum(lens[i] for dv in plan[1] for mb in dv for i in mb)}")
+for k, v in sorted(agg.items(), key=lambda x: -x[1])[:25]:
+    print(f"{v / tot * 100:5.1f}%  {v / 1e3:8.2f} ms  n={cnt[k]:5d}  {k}")
