@@ -77,7 +77,10 @@ class OdcEngine:
     def close(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            lib().odc_ctx_destroy(h)
+            try:
+                lib().odc_ctx_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self.h = C.c_void_p()
 
     __del__ = close

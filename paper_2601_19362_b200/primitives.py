@@ -131,7 +131,10 @@ class ShardFabric:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            lib().odc_fabric_destroy(h)
+            try:
+                lib().odc_fabric_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = C.c_void_p()
 
     def state(self) -> ShardState:
