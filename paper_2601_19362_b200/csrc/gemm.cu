@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -93,27 +94,36 @@ struct Args {
     int d_f32, accumulate;
     int a_mn, b_mn;  // 1 = MN-major operand
     int tiles_m, tiles_n;
+    int splits;  // split-K factor (fp32 output only): partial tiles are red.add-ed into D
 };
 
+template <int BN>
+__device__ __forceinline__ void tile_coords(int tile, const Args& g, int& m0, int& n0) {
+    // grouped rasterisation: 8 M-tiles share the same N-tiles for L2 reuse
+    constexpr int group = 8;
+    const int per_group = group * g.tiles_n;
+    const int gid = tile / per_group, first_m = gid * group;
+    const int gsize = min(group, g.tiles_m - first_m);
+    m0 = (first_m + (tile % per_group) % gsize) * BM;
+    n0 = ((tile % per_group) / gsize) * BN;
+}
+
+// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ... The TMEM
+// accumulator is double-buffered (2 x BN fp32 columns), so the epilogue of
+// tile i (warps 2..5) overlaps the MMAs of tile i+1 (warp 1) while warp 0
+// keeps the smem ring full across tile boundaries.
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Args g) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) unsigned long long full_bar[C::kStages], empty_bar[C::kStages], tmem_full;
+    __shared__ __align__(8) unsigned long long full_bar[C::kStages], empty_bar[C::kStages];
+    __shared__ __align__(8) unsigned long long tmem_full[2], tmem_empty[2];
     __shared__ unsigned tmem_base;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    // grouped rasterisation: 8 M-tiles share the same N-tiles for L2 reuse
-    const int tile = blockIdx.x;
-    const int group = 8;
-    const int per_group = group * g.tiles_n;
-    const int gid = tile / per_group, first_m = gid * group;
-    const int gsize = min(group, g.tiles_m - first_m);
-    const int tm = first_m + (tile % per_group) % gsize;
-    const int tn = (tile % per_group) / gsize;
-    const int m0 = tm * BM, n0 = tn * BN;
+    const int num_items = g.tiles_m * g.tiles_n * g.splits;
     const int k_tiles = static_cast<int>((g.K + BK - 1) / BK);
 
     if (warp == 0 && lane == 0) {
@@ -121,14 +131,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
-        mbar_init(&tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
-                     "n"(C::kTmemCols)
+                     "n"(2 * C::kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -139,24 +152,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
-            for (int kt = 0; kt < k_tiles; ++kt) {
-                const int s = kt % C::kStages;
-                if (kt >= C::kStages) mbar_wait(&empty_bar[s], ((kt / C::kStages) - 1) & 1);
-                char* sa = smem + s * C::kStageBytes;
-                char* sb = sa + C::kABytes;
-                mbar_expect_tx(&full_bar[s], C::kStageBytes);
-                const int k0 = kt * BK;
-                if (!g.a_mn) {
-                    tma_load_2d(&map_a, &full_bar[s], sa, k0, m0);
-                } else {
-                    tma_load_2d(&map_a, &full_bar[s], sa, m0, k0);
-                    tma_load_2d(&map_a, &full_bar[s], sa + 64 * BK * 2, m0 + 64, k0);
-                }
-                if (!g.b_mn) {
-                    tma_load_2d(&map_b, &full_bar[s], sb, k0, n0);
-                } else {
+            int it = 0;
+            for (int w = blockIdx.x; w < num_items; w += gridDim.x) {
+                int m0, n0;
+                tile_coords<BN>(w / g.splits, g, m0, n0);
+                const int sp = w % g.splits;
+                const int kb = k_tiles * sp / g.splits, ke = k_tiles * (sp + 1) / g.splits;
+                for (int kt = kb; kt < ke; ++kt, ++it) {
+                    const int s = it % C::kStages;
+                    if (it >= C::kStages) mbar_wait(&empty_bar[s], ((it / C::kStages) - 1) & 1);
+                    char* sa = smem + s * C::kStageBytes;
+                    char* sb = sa + C::kABytes;
+                    mbar_expect_tx(&full_bar[s], C::kStageBytes);
+                    const int k0 = kt * BK;
+                    if (!g.a_mn) {
+                        tma_load_2d(&map_a, &full_bar[s], sa, k0, m0);
+                    } else {
+                        tma_load_2d(&map_a, &full_bar[s], sa, m0, k0);
+                        tma_load_2d(&map_a, &full_bar[s], sa + 64 * BK * 2, m0 + 64, k0);
+                    }
+                    if (!g.b_mn) {
+                        tma_load_2d(&map_b, &full_bar[s], sb, k0, n0);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < BN / 64; ++j) tma_load_2d(&map_b, &full_bar[s], sb + j * 64 * BK * 2, n0 + 64 * j, k0);
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_2d(&map_b, &full_bar[s], sb + j * 64 * BK * 2, n0 + 64 * j, k0);
+                    }
                 }
             }
         }
@@ -168,100 +189,132 @@ __global__ void __launch_bounds__(kThreads, 1)
             //           next 64 MN at LBO = BK*128 B, k-step +2048 B
             const unsigned a_lbo = g.a_mn ? BK * 128 : 16, b_lbo = g.b_mn ? BK * 128 : 16;
             const unsigned a_step = g.a_mn ? 2048 : 32, b_step = g.b_mn ? 2048 : 32;
-            for (int kt = 0; kt < k_tiles; ++kt) {
-                const int s = kt % C::kStages;
-                mbar_wait(&full_bar[s], (kt / C::kStages) & 1);
+            int it = 0, j = 0;
+            for (int w = blockIdx.x; w < num_items; w += gridDim.x, ++j) {
+                const int sp = w % g.splits;
+                const int kb = k_tiles * sp / g.splits, ke = k_tiles * (sp + 1) / g.splits;
+                const int acc = j & 1, use = j >> 1;
+                if (use > 0) mbar_wait(&tmem_empty[acc], (use - 1) & 1);  // epilogue drained this buffer
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const unsigned sa = su32(smem + s * C::kStageBytes);
-                const unsigned sb = sa + C::kABytes;
+                const unsigned d_tmem = tmem + static_cast<unsigned>(acc * BN);
+                for (int kt = kb; kt < ke; ++kt, ++it) {
+                    const int s = it % C::kStages;
+                    mbar_wait(&full_bar[s], (it / C::kStages) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned sa = su32(smem + s * C::kStageBytes);
+                    const unsigned sb = sa + C::kABytes;
 #pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk) {
-                    const std::uint64_t da = smem_desc(sa + kk * a_step, a_lbo, 1024);
-                    const std::uint64_t db = smem_desc(sb + kk * b_step, b_lbo, 1024);
-                    const unsigned acc = (kt > 0 || kk > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem),
-                        "l"(da), "l"(db), "r"(idesc), "r"(acc)
-                        : "memory");
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const std::uint64_t da = smem_desc(sa + kk * a_step, a_lbo, 1024);
+                        const std::uint64_t db = smem_desc(sb + kk * b_step, b_lbo, 1024);
+                        const unsigned accum = (kt > kb || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+                            "l"(da), "l"(db), "r"(idesc), "r"(accum)
+                            : "memory");
+                    }
+                    // frees the smem stage once these MMAs have read it
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     su32(&empty_bar[s]))
+                                 : "memory");
                 }
-                // frees the smem stage once these MMAs have read it
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 su32(&empty_bar[s]))
+                                 su32(&tmem_full[acc]))
                              : "memory");
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             su32(&tmem_full))
-                         : "memory");
         }
     } else {  // ---- epilogue warps 2..5
-        mbar_wait(&tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int quad = warp % 4;  // TMEM lane quadrant this warp may access
-        const long long row = m0 + quad * 32 + lane;
-        const bool row_ok = row < g.M;
+        int j = 0;
+        for (int w = blockIdx.x; w < num_items; w += gridDim.x, ++j) {
+            const int acc = j & 1, use = j >> 1;
+            int m0, n0;
+            tile_coords<BN>(w / g.splits, g, m0, n0);
+            mbar_wait(&tmem_full[acc], use & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const long long row = m0 + quad * 32 + lane;
+            const bool row_ok = row < g.M;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-            unsigned r[32];
-            const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(c);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (!row_ok) continue;
-            const long long col0 = n0 + c;
-            if (col0 >= g.N) continue;
-            const bool full = col0 + 32 <= g.N;
-            if (g.d_f32) {
-                float* out = static_cast<float*>(g.D) + row * g.ldd + col0;
-                if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                               __uint_as_float(r[j + 3]));
-                        if (g.accumulate) {
-                            const float4 o = *reinterpret_cast<const float4*>(out + j);
-                            v.x += o.x;
-                            v.y += o.y;
-                            v.z += o.z;
-                            v.w += o.w;
-                        }
-                        *reinterpret_cast<float4*>(out + j) = v;
-                    }
-                } else {
-                    for (int j = 0; j < 32 && col0 + j < g.N; ++j)
-                        out[j] = __uint_as_float(r[j]) + (g.accumulate ? out[j] : 0.f);
+            for (int c = 0; c < BN; c += 32) {
+                unsigned r[32];
+                const unsigned taddr =
+                    tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN + c);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c + 32 >= BN) {  // whole accumulator now in registers: hand the buffer back early
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(&tmem_empty[acc])) : "memory");
                 }
-            } else {
-                __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + col0;
-                const __nv_bfloat16* add = g.C ? static_cast<const __nv_bfloat16*>(g.C) + row * g.ldd + col0
-                                               : (g.accumulate ? out : nullptr);
-                if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+                if (!row_ok) continue;
+                const long long col0 = n0 + c;
+                if (col0 >= g.N) continue;
+                const bool full = col0 + 32 <= g.N;
+                if (g.d_f32) {
+                    float* out = static_cast<float*>(g.D) + row * g.ldd + col0;
+                    if (g.splits > 1) {  // partial K range: reduce into D (zeroed or accumulated by the host)
+                        if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        uint4 v, a4 = make_uint4(0, 0, 0, 0);
-                        if (add) a4 = *reinterpret_cast<const uint4*>(add + j);
-                        const unsigned* aw = reinterpret_cast<const unsigned*>(&a4);
-                        unsigned* w = reinterpret_cast<unsigned*>(&v);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float lo = __uint_as_float(r[j + 2 * q]) + __uint_as_float(aw[q] << 16);
-                            const float hi = __uint_as_float(r[j + 2 * q + 1]) + __uint_as_float(aw[q] & 0xffff0000u);
-                            __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-                            w[q] = *reinterpret_cast<unsigned*>(&h);
+                            for (int q = 0; q < 32; q += 4)
+                                asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(out + q), "f"(__uint_as_float(r[q])),
+                                             "f"(__uint_as_float(r[q + 1])), "f"(__uint_as_float(r[q + 2])),
+                                             "f"(__uint_as_float(r[q + 3]))
+                                             : "memory");
+                        } else {
+                            for (int q = 0; q < 32 && col0 + q < g.N; ++q) atomicAdd(out + q, __uint_as_float(r[q]));
                         }
-                        *reinterpret_cast<uint4*>(out + j) = v;
+                    } else if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 4) {
+                            float4 v = make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]),
+                                                   __uint_as_float(r[q + 2]), __uint_as_float(r[q + 3]));
+                            if (g.accumulate) {
+                                const float4 o = *reinterpret_cast<const float4*>(out + q);
+                                v.x += o.x;
+                                v.y += o.y;
+                                v.z += o.z;
+                                v.w += o.w;
+                            }
+                            *reinterpret_cast<float4*>(out + q) = v;
+                        }
+                    } else {
+                        for (int q = 0; q < 32 && col0 + q < g.N; ++q)
+                            out[q] = __uint_as_float(r[q]) + (g.accumulate ? out[q] : 0.f);
                     }
                 } else {
-                    for (int j = 0; j < 32 && col0 + j < g.N; ++j) {
-                        float x = __uint_as_float(r[j]) + (add ? __bfloat162float(add[j]) : 0.f);
-                        out[j] = __float2bfloat16_rn(x);
+                    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + col0;
+                    const __nv_bfloat16* add = g.C ? static_cast<const __nv_bfloat16*>(g.C) + row * g.ldd + col0
+                                                   : (g.accumulate ? out : nullptr);
+                    if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 8) {
+                            uint4 v, a4 = make_uint4(0, 0, 0, 0);
+                            if (add) a4 = *reinterpret_cast<const uint4*>(add + q);
+                            const unsigned* aw = reinterpret_cast<const unsigned*>(&a4);
+                            unsigned* w = reinterpret_cast<unsigned*>(&v);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float lo = __uint_as_float(r[q + 2 * e]) + __uint_as_float(aw[e] << 16);
+                                const float hi = __uint_as_float(r[q + 2 * e + 1]) + __uint_as_float(aw[e] & 0xffff0000u);
+                                __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+                                w[e] = *reinterpret_cast<unsigned*>(&h);
+                            }
+                            *reinterpret_cast<uint4*>(out + q) = v;
+                        }
+                    } else {
+                        for (int q = 0; q < 32 && col0 + q < g.N; ++q) {
+                            float x = __uint_as_float(r[q]) + (add ? __bfloat162float(add[q]) : 0.f);
+                            out[q] = __float2bfloat16_rn(x);
+                        }
                     }
                 }
             }
@@ -271,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * C::kTmemCols)
                      : "memory");
     }
 }
@@ -324,8 +377,16 @@ cudaError_t launch(const void* A, const void* B, const Args& g, long long lda, l
     // A: K-major [M][K] (box 64 x 128) or M-major [K][M] (box 64 x 64)
     CUtensorMap ma = g.a_mn ? make_map(A, g.M, g.K, lda, 64, BK) : make_map(A, g.K, g.M, lda, BK, BM);
     CUtensorMap mb = g.b_mn ? make_map(B, g.N, g.K, ldb, 64, BK) : make_map(B, g.K, g.N, ldb, BK, BN);
+    static int sms = 0;
+    if (!sms) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (const char* r = std::getenv("ODC_GEMM_RESERVE_SMS")) sms -= std::atoi(r);  // leave SMs to comm kernels
+        if (sms < 1) sms = 1;
+    }
+    const int tiles = g.tiles_m * g.tiles_n;
+    const int items = tiles * g.splits;
     count_launch();
-    gemm_kernel<BN><<<g.tiles_m * g.tiles_n, kThreads, C::kSmem, s>>>(ma, mb, g);
+    gemm_kernel<BN><<<items < sms ? items : sms, kThreads, C::kSmem, s>>>(ma, mb, g);
     return cudaGetLastError();
 }
 
@@ -355,13 +416,33 @@ extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const
         g.a_mn = a_mn_major ? 1 : 0;
         g.b_mn = b_mn_major ? 1 : 0;
         g.tiles_m = static_cast<int>((M + odc::gemm::BM - 1) / odc::gemm::BM);
+        // split-K for fp32 outputs whose tile count cannot fill the GPU (wgrad of
+        // d x d weights): partial tiles are reduced with red.global.add.v4.f32
+        g.splits = 1;
+        {
+            const long long bn = N <= 128 ? 128 : 256;
+            const long long tiles = g.tiles_m * ((N + bn - 1) / bn);
+            const long long kt = (K + odc::gemm::BK - 1) / odc::gemm::BK;
+            if (g.d_f32 && tiles < 120 && kt >= 8) {
+                long long sp = (148 + tiles - 1) / tiles;
+                sp = sp > 4 ? 4 : sp;
+                sp = sp > kt / 4 ? kt / 4 : sp;
+                g.splits = static_cast<int>(sp < 1 ? 1 : sp);
+            }
+        }
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (g.splits > 1 && !accumulate) {
+            cudaError_t z = cudaMemset2DAsync(D, static_cast<size_t>(ldd) * 4, 0, static_cast<size_t>(N) * 4,
+                                              static_cast<size_t>(M), st);
+            if (z != cudaSuccess) throw std::runtime_error(std::string("gemm split-K zero: ") + cudaGetErrorString(z));
+        }
         cudaError_t e;
         if (N <= 128) {
             g.tiles_n = static_cast<int>((N + 127) / 128);
-            e = odc::gemm::launch<128>(A, B, g, lda, ldb, reinterpret_cast<cudaStream_t>(stream));
+            e = odc::gemm::launch<128>(A, B, g, lda, ldb, st);
         } else {
             g.tiles_n = static_cast<int>((N + 255) / 256);
-            e = odc::gemm::launch<256>(A, B, g, lda, ldb, reinterpret_cast<cudaStream_t>(stream));
+            e = odc::gemm::launch<256>(A, B, g, lda, ldb, st);
         }
         if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
     });

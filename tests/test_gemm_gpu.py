@@ -16,7 +16,7 @@ def _r(*s):
 
 
 @pytest.mark.parametrize("T,inn,out", [(128, 64, 128), (1000, 1536, 256), (4096, 1536, 8960), (333, 8960, 1536),
-                                       (257, 192, 320)])
+                                       (257, 192, 320), (4096, 256, 384), (16384, 1536, 1536)])
 def test_fwd_dgrad_wgrad(T, inn, out):
     x, w, dy = _r(T, inn), _r(out, inn), _r(T, out)
     y = G.linear_fwd(x, w)
