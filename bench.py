@@ -358,6 +358,7 @@ def run_sft(args):
 
     if args.trace:
         write_trace(args.trace, shape, W.OdcComm(eng), plan_odc, lens, timed_steps[0], rank, world, dev)
+    comm = comm_rates(eng, sizes[1], rank, world, dev)
 
     hbm, hbm_kind = peaks()
     try:
@@ -395,7 +396,7 @@ def run_sft(args):
                              "analytic_compute_only_speedup": round(pred[0], 4),
                              "analytic_bubble_odc_lbmini": round(pred[1], 4),
                              "analytic_bubble_fsdp_lbmicro": round(pred[2], 4)} if fs else None),
-                "roofline": roof, "clocks": clk.summary(),
+                "roofline": roof, "fetch_push": comm, "clocks": clk.summary(),
                 "e2e": ({"value": round(e2e["tps"], 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / args.steps),
                          "d2h_bytes_per_step": 4, "loss": e2e["loss"],
                          "note": "token ids/labels/positions built on host per microbatch, copied H2D inside the "
@@ -405,6 +406,46 @@ def run_sft(args):
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def comm_rates(eng, M, rank, world, dev, reps=10):
+    """fetch / push GB/s of one transformer-layer unit with every rank
+    fetching (then pushing) concurrently, CUDA events on the launching stream,
+    max over ranks. Bytes: N>1 the NVLink share ((N-1)*block*2 B fetch,
+    (N-1)*block*4 B push, per direction); N=1 the local HBM bytes."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_19362_b200.dist import rank_timings
+
+    out = torch.empty(M, dtype=torch.bfloat16, device=dev)
+    grad = torch.full((M,), 1e-6, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    res = {}
+    for name, fn in (("fetch", lambda: eng.fetch(1, out)), ("push", lambda: eng.push(1, grad, 1.0))):
+        fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms, _, _, _ = rank_timings(a.elapsed_time(b) / reps, 0.0, 0, device=dev)
+        block = (M + world - 1) // world
+        if world > 1:
+            nbytes = (world - 1) * block * (2 if name == "fetch" else 4)
+        else:
+            nbytes = M * (4 if name == "fetch" else 12)
+        res[name + "_GBps"] = round(nbytes / (ms / 1e3) / 1e9, 1)
+        res[name + "_us"] = round(ms * 1e3, 1)
+    peak = NVLINK_NOMINAL_GBS if world > 1 else peaks()[0]
+    res.update({"bytes": "NVLink per direction" if world > 1 else "local HBM read+write", "peak_GBps": peak,
+                "fetch_frac": round(res["fetch_GBps"] / peak, 4), "push_frac": round(res["push_GBps"] / peak, 4),
+                "unit_elems": M, "all_ranks_concurrent": True})
+    return res
 
 
 def write_trace(path, shape, comm, plan, lens, k, rank, world, dev):

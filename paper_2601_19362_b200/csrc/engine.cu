@@ -150,7 +150,12 @@ void launch_fetch(const odc_ctx* c, const odc::SegTable& t, cudaStream_t s) {
                             "fetch (ce)");
             return;
         }
-        default: cuda_ok(odc::launch_fetch_tma(t, c->cfg.fetch_ctas, s), "fetch (tma)");
+        default: {
+            // all-local fetch (N=1) is HBM-bound: give it the whole GPU; over
+            // NVLink 64 CTAs already saturate the link (profiles/r01/p2p_*)
+            const int ctas = c->cfg.fetch_ctas > 0 ? c->cfg.fetch_ctas : (c->world() == 1 ? 148 : 64);
+            cuda_ok(odc::launch_fetch_tma(t, ctas, s), "fetch (tma)");
+        }
     }
 }
 
