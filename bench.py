@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--workload", default="sft", choices=["sft", "odc_minibatch_comm"])
     ap.add_argument("--no-fsdp", action="store_true", help="skip the same-box NCCL FSDP comparison arm")
     ap.add_argument("--trace", default="", help="write a Chrome trace (reference schema) of one extra ODC step")
+    ap.add_argument("--cost", default="b200", choices=["b200", "flops"],
+                    help="LB cost beta/alpha: FLOP ratio ('flops') or FLOP ratio x measured kernel-throughput ratio")
+    ap.add_argument("--cache-params", action="store_true",
+                    help="SURVEY 8(f)1: keep fetched units for the whole minibatch (one fetch per unit per step)")
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--push-mode", default="red", choices=["red", "slot"])
     ap.add_argument("--minibs", type=int, default=8)
@@ -260,7 +264,7 @@ def run_sft(args):
     shape = SHAPES[args.model]
     sizes = W.unit_sizes(shape)
     lens = workload_lengths()
-    beta = shape.beta_over_alpha()
+    beta = shape.beta_over_alpha_b200() if args.cost == "b200" else shape.beta_over_alpha()
     cost = P.CostModel(1.0, beta, 1)
     plan_odc = P.plan_flat("lb-mini", lens, world, args.minibs, 32768, cost)
     plan_fsdp = P.plan_flat("lb-micro", lens, world, args.minibs, 32768, cost)
@@ -287,7 +291,7 @@ def run_sft(args):
         return sum(lens[i] for dv in plan[k % len(plan)] for mb in dv for i in mb)
 
     def run_arm(comm, plan, resident: bool, record=False, clocks=None):
-        worker = W.Worker(shape, comm, dev)
+        worker = W.Worker(shape, comm, dev, cache_params=args.cache_params and comm.name == "odc")
         stream = torch.cuda.current_stream()
 
         def one(k, batches=None):
@@ -389,6 +393,8 @@ def run_sft(args):
                            "minibs_per_rank": args.minibs, "budget_tokens": 32768,
                            "lengths": "lognormal(8,1.5) n=2048 cap=32768 seed=0, floor 512",
                            "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
+                           "cost_beta_over_alpha": round(beta, 1), "cost_model": args.cost,
+                           "cache_params": args.cache_params,
                            "tokens_timed": res["tokens"], "l2": "inputs > L2 (GBs of activations/units), no flush"},
                 "idle_fraction": round(res["idle"], 4),
                 "idle_note": "1 - sum(busy)/(N*T), busy = device time from step start to the minibatch barrier",

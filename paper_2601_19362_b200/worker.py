@@ -258,7 +258,8 @@ def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, devic
 
 
 class Worker:
-    def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192, max_positions: int = 65536):
+    def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192, max_positions: int = 65536,
+                 cache_params: bool = False):
         if _flash_attn_varlen_forward is None:
             raise ImportError("flash-attn (sm_100) is required for the worker's attention")
         self.s, self.comm, self.dev = shape, comm, torch.device(device)
@@ -273,8 +274,29 @@ class Worker:
         self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
         self.rope = F.rope_table(max_positions, shape.head_dim, ROPE_THETA, self.dev)
         self.tracer: Optional[Tracer] = None
+        # parameters cannot change inside a minibatch, so with
+        # HBM to spare every unit is fetched once per minibatch and reused by
+        # the backward and by later microbatches (ODC only: FSDP reshards)
+        self.cache = None
+        if cache_params:
+            self.cache = [self.ebuf] + [torch.empty(lsz, dtype=torch.bfloat16, device=self.dev) for _ in range(self.L)]
+            self.cache_ev = [None] * (self.L + 1)
 
     # --- stream helpers
+    def _ubuf(self, unit):
+        if self.cache is not None:
+            return self.cache[unit]
+        return self.ebuf if unit == 0 else self.pbuf[unit % 2]
+
+    def _fetch_unit(self, unit, after: Optional[torch.cuda.Event] = None):
+        if self.cache is not None and self.cache_ev[unit] is not None:
+            return self.cache_ev[unit]  # already resident for this minibatch
+        # a cached unit has its own buffer: no need to wait for compute to release one
+        ev = self._fetch(unit, self._ubuf(unit), None if self.cache is not None else after)
+        if self.cache is not None:
+            self.cache_ev[unit] = ev
+        return ev
+
     def _fetch(self, unit, buf, after: Optional[torch.cuda.Event] = None):
         if after is not None:
             self.comm_stream.wait_event(after)
@@ -296,17 +318,17 @@ class Worker:
         tab = self.rope
 
         # ---------------- forward
-        ev_e = self._fetch(0, self.ebuf, after=_record(cur))
-        ev = self._fetch(1, self.pbuf[1 % 2], after=_record(cur))
+        ev_e = self._fetch_unit(0, after=_record(cur))
+        ev = self._fetch_unit(1, after=_record(cur))
         cur.wait_event(ev_e)
-        E = views(self.ebuf, embed_layout(s))
+        E = views(self._ubuf(0), embed_layout(s))
         h = E["emb"].index_select(0, b.ids)
         saved = []
         for l in range(1, L + 1):
             cur.wait_event(ev)
-            P = views(self.pbuf[l % 2], lay)
+            P = views(self._ubuf(l), lay)
             if l < L:  # prefetch the next unit into the other buffer once layer l-1 released it
-                ev = self._fetch(l + 1, self.pbuf[(l + 1) % 2], after=_record(cur))
+                ev = self._fetch_unit(l + 1, after=_record(cur))
             x = h
             tr = self.tracer.span("fwd", l, cur, False) if self.tracer else None
             a, r1 = F.rmsnorm_fwd(x, P["ln1"])
@@ -345,13 +367,17 @@ class Worker:
         del dhf, hf
 
         # ---------------- backward through the layers
-        ev = self._fetch(L, self.pbuf[L % 2], after=_record(cur))
+        if self.cache is None:  # the forward's buffers were recycled: re-fetch (FSDP semantics)
+            ev = self._fetch(L, self.pbuf[L % 2], after=_record(cur))
+        else:
+            ev = self._fetch_unit(L)
         push_ev = [None, None]
         for l in range(L, 0, -1):
             cur.wait_event(ev)
-            P = views(self.pbuf[l % 2], lay)
+            P = views(self._ubuf(l), lay)
             if l > 1:
-                ev = self._fetch(l - 1, self.pbuf[(l - 1) % 2], after=_record(cur))
+                ev = (self._fetch(l - 1, self.pbuf[(l - 1) % 2], after=_record(cur)) if self.cache is None
+                      else self._fetch_unit(l - 1))
             gi = l % 2
             if push_ev[gi] is not None:  # grad buffer free once its previous push finished
                 cur.wait_event(push_ev[gi])
@@ -425,6 +451,8 @@ class Worker:
         cur.wait_event(_record(self.comm_stream))
 
     def minibatch_end(self, lr=1e-5):
+        if self.cache is not None:  # new parameter epoch: every unit must be fetched again
+            self.cache_ev = [None] * (self.L + 1)
         cur = torch.cuda.current_stream(self.dev)
         self.comm_stream.wait_event(_record(cur))
         self.comm.minibatch_end(self.comm_stream)

@@ -90,3 +90,28 @@ def test_worker_matches_fp32_reference():
         cos = F.cosine_similarity(got, want, dim=0).item()
         rel = ((got - want).norm() / want.norm()).item()
         assert cos > 0.995 and rel < 5e-2, (u, cos, rel)
+
+
+def test_param_cache_matches_refetch():
+    """with cache_params the worker fetches each unit once per
+    minibatch; gradients over two microbatches must match the re-fetch path."""
+    s = TINY
+    sizes = W.unit_sizes(s)
+    gen = torch.Generator(device=DEV).manual_seed(1)
+    units = [W.init_unit(s, u, gen, DEV) for u in range(len(sizes))]
+    lens = [37, 100, 63, 200]
+    grads = []
+    for cache in (False, True):
+        eng = OdcEngine(sizes, push_mode="slot")
+        for u, t in enumerate(units):
+            eng.set_params(u, t)
+        wk = W.Worker(s, W.OdcComm(eng), DEV, ce_chunk=128, cache_params=cache)
+        for mb in ([0, 1], [2, 3]):
+            wk.microbatch(W.make_batch(lens, mb, s.vocab, DEV), 0.5)
+        eng.minibatch_end()
+        eng.check()
+        grads.append([eng.read_grad_shard(u).clone() for u in range(len(sizes))])
+    # the glue kernels reduce with atomics (dw, bias grads, split-K), so two
+    # runs agree to fp32 rounding, not bitwise
+    for a, b in zip(*grads):
+        torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-7)
