@@ -33,6 +33,12 @@ def step(k):
 
 step(0)
 torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+step(1)
+b.record()
+torch.cuda.synchronize()
+print(f"step wall (device events) {a.elapsed_time(b):.1f} ms")
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
     step(1)
     torch.cuda.synchronize()
