@@ -201,6 +201,13 @@ odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, i
                          int64_t lda, int64_t ldb, int64_t ldd, int a_mn_major, int b_mn_major, int d_dtype,
                          int accumulate, void* stream);
 
+/* Causal varlen flash-attention forward on tcgen05 (head_dim 128, GQA).
+ * q [T][H][128], k/v [T][KV][128] bf16; out [T][H][128]; lse [H][T] fp32 (natural log).
+ * items: n_items x {seq_start, seq_len, q_tile, head} (int32 x4), one CTA each;
+ * order heaviest (most KV tiles) first. */
+odc_status odc_attn_fwd(const void* q, const void* k, const void* v, void* out, float* lse, const void* items,
+                        int n_items, int64_t T, int H, int KV, int head_dim, float scale, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Fused elementwise kernels of the SFT worker (csrc/worker_kernels.cu).
  * bf16 tensors row-major and 16-byte aligned; fp32 for rstd / dw / loss.

@@ -1,0 +1,405 @@
+// attention.cu — causal varlen flash-attention FORWARD on tcgen05 (the
+// worker's attention; no reference counterpart — the reference models its
+// cost as alpha*s^2, src/cost_model.cpp:14-18). head_dim 128, bf16 in/out,
+// fp32 softmax statistics, GQA (H query heads share H/KV kv heads).
+//
+// One CTA per (sequence, 128-query tile, query head), heaviest items first.
+//   warp 0     TMA: Q tile once; K_j / V_j tiles through a 2-stage ring.
+//              K and V use the same box {64 hd, 128 keys}: K is read as a
+//              K-major B operand (S = Q K^T), V as an MN-major B (O += P V).
+//   warp 1     single-thread tcgen05.mma issuer: S_{j+1} = Q K_{j+1}^T into
+//              the other TMEM S buffer while the softmax warps work on S_j,
+//              then O += P_j V_j (O accumulates in TMEM).
+//   warps 2-5  softmax, one query row per thread: tcgen05.ld S, causal /
+//              sequence-end mask, online max/sum in the exp2 domain with lazy
+//              rescaling (O is rescaled in TMEM only when the running max grows
+//              by more than 2^8), P (bf16) written to smem in the 128B-swizzled
+//              K-major layout the MMA reads; finally O / l -> bf16, and LSE.
+// TMEM: S0 [0,128) S1 [128,256) O [256,384) of 512 columns.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace odc {
+namespace attn {
+
+constexpr int HD = 128;
+constexpr int BQ = 128, BKV = 128;
+constexpr int kThreads = 192;
+constexpr int kTile = BQ * HD * 2;              // 32 KB: one 128 x 128 bf16 tile (two 16 KB swizzle halves)
+constexpr int kSmem = kTile * 6 + 1024;         // Q, K x2, V x2, P
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;       // log2 units
+
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, unsigned long long* bar, void* smem, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(smem)),
+        "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ std::uint64_t sdesc(unsigned addr, unsigned lbo, unsigned sbo) {
+    std::uint64_t d = static_cast<std::uint64_t>((addr & 0x3FFFF) >> 4);
+    d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;
+    d |= 2ull << 61;
+    return d;
+}
+// bf16 x bf16 -> f32, M=128, N=128
+__host__ __device__ constexpr unsigned idesc(int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(b_mn_major) << 16) | ((128u >> 3) << 17) |
+           ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void mma(unsigned d, std::uint64_t a, std::uint64_t b, unsigned id, unsigned acc) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+
+#define TM_LD32(taddr, r)                                                                                        \
+    asm volatile(                                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                       \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),      \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),            \
+          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),            \
+          "=r"(r[30]), "=r"(r[31])                                                                               \
+        : "r"(taddr))
+#define TM_ST32(taddr, r)                                                                                          \
+    asm volatile(                                                                                                  \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                              \
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),        \
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), \
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]),           \
+        "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                                     \
+        : "memory")
+
+struct Item {
+    int seq_start, seq_len, q_tile, head;
+};
+
+struct Args {
+    const Item* items;
+    int n_items;
+    int H, KV;
+    float scale_log2;  // softmax scale * log2(e)
+    __nv_bfloat16* out;  // [T][H][HD]
+    float* lse;          // [H][T] natural-log LSE
+    long long T;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, Args g) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    char* sQ = smem;
+    char* sK[2] = {smem + kTile, smem + 2 * kTile};
+    char* sV[2] = {smem + 3 * kTile, smem + 4 * kTile};
+    char* sP = smem + 5 * kTile;
+    __shared__ __align__(8) unsigned long long q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, pv_done;
+    __shared__ unsigned tmem_base;
+
+    const Item it = g.items[blockIdx.x];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int kvh = it.head / (g.H / g.KV);
+    const int q0 = it.q_tile * BQ;                        // first query row within the sequence
+    const int n_kv = min((it.seq_len + BKV - 1) / BKV, it.q_tile + 1);  // causal: keys <= last query
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(&q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_free[s], 4);
+        }
+        mbar_init(&p_full, 4);
+        mbar_init(&pv_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_q) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_v) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA
+            const int row0 = it.seq_start + q0;
+            mbar_expect_tx(&q_full, kTile);
+            tma_2d(&map_q, &q_full, sQ, it.head * HD, row0);
+            tma_2d(&map_q, &q_full, sQ + kTile / 2, it.head * HD + 64, row0);
+            for (int j = 0; j < n_kv; ++j) {
+                const int s = j & 1;
+                if (j >= 2) mbar_wait(&kv_empty[s], ((j >> 1) - 1) & 1);
+                const int k0 = it.seq_start + j * BKV;
+                mbar_expect_tx(&kv_full[s], 2 * kTile);
+                tma_2d(&map_k, &kv_full[s], sK[s], kvh * HD, k0);
+                tma_2d(&map_k, &kv_full[s], sK[s] + kTile / 2, kvh * HD + 64, k0);
+                tma_2d(&map_v, &kv_full[s], sV[s], kvh * HD, k0);
+                tma_2d(&map_v, &kv_full[s], sV[s] + kTile / 2, kvh * HD + 64, k0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const unsigned id_qk = idesc(0), id_pv = idesc(1);
+            mbar_wait(&q_full, 0);
+            auto issue_s = [&](int j) {
+                const int s = j & 1;
+                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                if (j >= 2) mbar_wait(&s_free[s], ((j >> 1) - 1) & 1);  // softmax finished reading S_{j-2}
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned qa = su32(sQ), ka = su32(sK[s]);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {  // K dim = head dim, two 64-wide swizzle halves
+                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + s * 128, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_qk, kk > 0);
+                }
+                commit(&s_full[s]);
+            };
+            issue_s(0);
+            for (int j = 0; j < n_kv; ++j) {
+                if (j + 1 < n_kv) issue_s(j + 1);
+                mbar_wait(&p_full, j & 1);  // P_j in smem (and O rescaled)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const int s = j & 1;
+                const unsigned pa = su32(sP), va = su32(sV[s]);
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {  // K dim = keys
+                    const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;  // P: K-major
+                    const unsigned boff = kk * 2048;                                // V: MN-major, 16 key rows
+                    mma(tmem + 256, sdesc(pa + aoff, 16, 1024), sdesc(va + boff, kTile / 2, 1024), id_pv, (j > 0 || kk > 0));
+                }
+                commit(&kv_empty[s]);  // K_j, V_j consumed
+                commit(&pv_done);      // P buffer free, O stable
+            }
+        }
+    } else {  // ---- softmax / correction / epilogue (warps 2..5)
+        const int quad = warp % 4;
+        const int r = quad * 32 + lane;  // query row within the tile
+        const int qi = q0 + r;           // query index within the sequence
+        const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < n_kv; ++j) {
+            const int s = j & 1;
+            mbar_wait(&s_full[s], (j >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // the whole S row in registers: 4 TMEM loads in flight, one wait
+            unsigned v[128];
+            TM_LD32(tmem + lane_base + s * 128 + 0, (v + 0));
+            TM_LD32(tmem + lane_base + s * 128 + 32, (v + 32));
+            TM_LD32(tmem + lane_base + s * 128 + 64, (v + 64));
+            TM_LD32(tmem + lane_base + s * 128 + 96, (v + 96));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[s]);  // S buffer reusable for S_{j+2}
+            const int kbase = j * BKV;
+            // keys e <= lim are visible to this query (causal + sequence end)
+            const int lim = min(qi, it.seq_len - 1) - kbase;
+            float mx = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 128; ++e) {
+                const float x = __uint_as_float(v[e]) * g.scale_log2;
+                v[e] = __float_as_uint(e <= lim ? x : -INFINITY);
+                mx = fmaxf(mx, __uint_as_float(v[e]));
+            }
+            float m_new = m;
+            if (mx > m + kRescaleThreshold || m == -INFINITY) m_new = fmaxf(mx, m);
+            // P_{j-1} consumed and O_{j-1} complete before we touch P / O
+            if (j > 0) mbar_wait(&pv_done, (j - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (j > 0 && m_new != m) {  // lazy rescale of the running output in TMEM
+                const float alpha = ex2(m - m_new);
+                l *= alpha;
+#pragma unroll 1
+                for (int c = 0; c < HD; c += 32) {  // chunked: S row stays in registers
+                    unsigned o[32];
+                    TM_LD32(tmem + lane_base + 256 + c, o);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    TM_ST32(tmem + lane_base + 256 + c, o);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            m = m_new;
+            const float mm = (m == -INFINITY) ? 0.f : m;
+            // p = exp2(x - m) -> bf16 P in smem (128B-swizzled K-major), row sum of what the MMA sees
+#pragma unroll
+            for (int c = 0; c < BKV; c += 32) {
+                unsigned pk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const float p0 = ex2(__uint_as_float(v[c + e]) - mm);
+                    const float p1 = ex2(__uint_as_float(v[c + e + 1]) - mm);
+                    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+                    l += __low2float(h) + __high2float(h);
+                    pk[e / 2] = *reinterpret_cast<unsigned*>(&h);
+                }
+                char* half = sP + (c >> 6) * (kTile / 2) + r * 128;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int chunk = ((c & 63) >> 3) + q;
+                    *reinterpret_cast<uint4*>(half + ((chunk ^ (r & 7)) << 4)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full);
+        }
+        // epilogue: O / l -> bf16, LSE
+        mbar_wait(&pv_done, (n_kv - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const bool valid = qi < it.seq_len;
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const long long tok = static_cast<long long>(it.seq_start) + qi;
+        __nv_bfloat16* orow = g.out + (tok * g.H + it.head) * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+            unsigned v[32];
+            TM_LD32(tmem + lane_base + 256 + c, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (valid) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 o;
+                    unsigned* w = reinterpret_cast<unsigned*>(&o);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * q + 2 * e]) * inv,
+                                                                 __uint_as_float(v[8 * q + 2 * e + 1]) * inv);
+                        w[e] = *reinterpret_cast<unsigned*>(&h);
+                    }
+                    *reinterpret_cast<uint4*>(orow + c + 8 * q) = o;
+                }
+            }
+        }
+        if (valid) g.lse[static_cast<long long>(it.head) * g.T + tok] = (m + log2f(l)) / kLog2e;  // natural log
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap rows_map(const void* base, long long cols, long long rows) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw odcsim::ParamError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+}  // namespace attn
+}  // namespace odc
+
+extern "C" odc_status odc_attn_fwd(const void* q, const void* k, const void* v, void* out, float* lse, const void* items,
+                                   int n_items, std::int64_t T, int H, int KV, int head_dim, float scale, void* stream) {
+    return odc::guard([&] {
+        using namespace odc::attn;
+        if (head_dim != HD) throw odcsim::ParamError("attn_fwd: head_dim must be 128");
+        if (KV < 1 || H % KV) throw odcsim::ParamError("attn_fwd: H must be a multiple of KV");
+        if (n_items <= 0) return;
+        static thread_local int configured = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (configured != dev) {
+            cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            if (e != cudaSuccess) throw std::runtime_error(std::string("attn smem attr: ") + cudaGetErrorString(e));
+            configured = dev;
+        }
+        // q: [T][H*HD], k / v: [T][KV*HD] (the RoPE kernel's outputs)
+        CUtensorMap mq = rows_map(q, static_cast<long long>(H) * HD, T);
+        CUtensorMap mk = rows_map(k, static_cast<long long>(KV) * HD, T);
+        CUtensorMap mv = rows_map(v, static_cast<long long>(KV) * HD, T);
+        Args a{};
+        a.items = static_cast<const Item*>(items);
+        a.n_items = n_items;
+        a.H = H;
+        a.KV = KV;
+        a.scale_log2 = scale * kLog2e;
+        a.out = static_cast<__nv_bfloat16*>(out);
+        a.lse = lse;
+        a.T = T;
+        odc::count_launch();
+        attn_fwd_kernel<<<n_items, kThreads, kSmem, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw std::runtime_error(std::string("attn_fwd launch: ") + cudaGetErrorString(e));
+    });
+}

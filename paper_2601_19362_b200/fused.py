@@ -79,3 +79,27 @@ def ce_fwd_bwd_(logits, labels, scale, loss_accum):
     rows, V = logits.shape
     check(lib().odc_w_ce_fwd_bwd(_p(logits), _p(labels), rows, V, float(scale), _p(loss_accum), _s()))
     return logits
+
+
+def attn_items(lens, H: int, device) -> torch.Tensor:
+    """Work list of the tcgen05 attention forward: one item per (sequence,
+    128-query tile, head), heaviest (most causal KV tiles) first."""
+    items, start = [], 0
+    for n in lens:
+        for qt in range((n + 127) // 128):
+            for h in range(H):
+                items.append((start, n, qt, h))
+        start += n
+    items.sort(key=lambda t: -t[2])
+    return torch.tensor(items, dtype=torch.int32).to(device, non_blocking=True)
+
+
+def attn_fwd(q, k, v, items, scale):
+    """causal varlen attention, q [T,H,128], k/v [T,KV,128] -> out [T,H,128], lse [H,T]."""
+    T, H, hd = q.shape
+    KV = k.shape[1]
+    out = torch.empty_like(q)
+    lse = torch.empty(H, T, dtype=torch.float32, device=q.device)
+    check(lib().odc_attn_fwd(_p(q), _p(k), _p(v), _p(out), _p(lse), _p(items), items.shape[0], T, H, KV, hd,
+                             float(scale), _s()))
+    return out, lse

@@ -234,9 +234,10 @@ class Batch:
     cu_seqlens: torch.Tensor  # [n+1] int32
     max_len: int
     tokens: int
+    attn_items: Optional[torch.Tensor] = None  # tcgen05 attention work list (built per microbatch)
 
 
-def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, device) -> Batch:
+def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, device, heads: int = 0) -> Batch:
     """Synthetic packed microbatch: token ids seeded by the global sample id, so
     every implementation sees identical data."""
     ids, labels, pos, cu = [], [], [], [0]
@@ -251,15 +252,23 @@ def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, devic
         pos.append(torch.arange(n))
         cu.append(cu[-1] + n)
     T = cu[-1]
-    return Batch(torch.cat(ids).to(device, non_blocking=True), torch.cat(labels).to(device, non_blocking=True),
-                 torch.cat(pos).to(device, non_blocking=True),
-                 torch.tensor(cu, dtype=torch.int32).to(device, non_blocking=True),
-                 max(int(lens[s]) for s in sample_ids), T)
+    b = Batch(torch.cat(ids).to(device, non_blocking=True), torch.cat(labels).to(device, non_blocking=True),
+              torch.cat(pos).to(device, non_blocking=True),
+              torch.tensor(cu, dtype=torch.int32).to(device, non_blocking=True),
+              max(int(lens[s]) for s in sample_ids), T)
+    if heads:
+        attach_attn_items(b, [int(lens[s]) for s in sample_ids], heads, device)
+    return b
+
+
+def attach_attn_items(b: Batch, seq_lens: Sequence[int], heads: int, device) -> Batch:
+    b.attn_items = F.attn_items(list(seq_lens), heads, device)
+    return b
 
 
 class Worker:
     def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192, max_positions: int = 65536,
-                 cache_params: bool = False):
+                 cache_params: bool = False, attn: str = "tcgen05"):
         if _flash_attn_varlen_forward is None:
             raise ImportError("flash-attn (sm_100) is required for the worker's attention")
         self.s, self.comm, self.dev = shape, comm, torch.device(device)
@@ -274,6 +283,8 @@ class Worker:
         self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
         self.rope = F.rope_table(max_positions, shape.head_dim, ROPE_THETA, self.dev)
         self.tracer: Optional[Tracer] = None
+        # attention forward: own tcgen05 kernel (csrc/attention.cu) or flash-attn; backward: flash-attn
+        self.attn = attn if shape.head_dim == 128 else "flash"
         # parameters cannot change inside a minibatch, so with
         # HBM to spare every unit is fetched once per minibatch and reused by
         # the backward and by later microbatches (ODC only: FSDP reshards)
@@ -316,6 +327,9 @@ class Worker:
         scale = 1.0 / math.sqrt(hd)
         lay = layer_layout(s)
         tab = self.rope
+        if self.attn == "tcgen05" and b.attn_items is None:
+            cu = b.cu_seqlens.tolist()
+            attach_attn_items(b, [cu[i + 1] - cu[i] for i in range(len(cu) - 1)], H, self.dev)
 
         # ---------------- forward
         ev_e = self._fetch_unit(0, after=_record(cur))
@@ -335,8 +349,11 @@ class Worker:
             qkv = G.linear_fwd(a, P["qkv_w"])
             q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), tab, b.positions, H, KV, hd)
             del qkv
-            o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len, 0.0,
-                                                      scale, True)
+            if self.attn == "tcgen05":
+                o, lse = F.attn_fwd(q, k, v, b.attn_items, scale)
+            else:
+                o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len,
+                                                          0.0, scale, True)
             hm = G.linear_fwd(o.view(T, H * hd), P["o_w"], residual=x)
             bn, r2 = F.rmsnorm_fwd(hm, P["ln2"])
             gu = G.linear_fwd(bn, P["gu_w"])

@@ -1,0 +1,58 @@
+"""tcgen05 causal varlen attention forward vs flash-attn 2.8 (library) and a
+plain fp32 torch reference: out within bf16 tolerance (2e-2), LSE within 1e-3."""
+import pytest
+import torch
+import torch.nn.functional as TF
+
+from paper_2601_19362_b200 import fused as F
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _ref(q, k, v, lens, scale):
+    outs, lses, s0 = [], [], 0
+    H, KV = q.shape[1], k.shape[1]
+    for n in lens:
+        qs = q[s0:s0 + n].float().transpose(0, 1)
+        ks = k[s0:s0 + n].float().transpose(0, 1).repeat_interleave(H // KV, 0)
+        vs = v[s0:s0 + n].float().transpose(0, 1).repeat_interleave(H // KV, 0)
+        sc = qs @ ks.transpose(1, 2) * scale
+        mask = torch.triu(torch.ones(n, n, dtype=torch.bool, device=q.device), 1)
+        sc.masked_fill_(mask, float("-inf"))
+        lses.append(torch.logsumexp(sc, -1))
+        outs.append((torch.softmax(sc, -1) @ vs).transpose(0, 1))
+        s0 += n
+    return torch.cat(outs, 0), torch.cat(lses, 1)
+
+
+@pytest.mark.parametrize("lens,H,KV", [([128], 2, 1), ([1], 2, 2), ([300, 77, 513], 12, 2), ([1000, 2048], 4, 2),
+                                       ([129, 255, 256, 257], 6, 3)])
+def test_attn_fwd_matches_reference(lens, H, KV):
+    torch.manual_seed(0)
+    T = sum(lens)
+    q = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
+    k = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    v = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    scale = 128 ** -0.5
+    items = F.attn_items(lens, H, DEV)
+    out, lse = F.attn_fwd(q, k, v, items, scale)
+    ro, rl = _ref(q, k, v, lens, scale)
+    torch.testing.assert_close(out.float(), ro, rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(lse, rl, rtol=1e-3, atol=1e-3)
+
+
+def test_attn_fwd_matches_flash_attn_long():
+    from flash_attn.flash_attn_interface import _flash_attn_varlen_forward
+
+    torch.manual_seed(1)
+    lens = [8192, 3000, 700]
+    T, H, KV = sum(lens), 12, 2
+    q = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
+    k = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    v = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    cu = torch.tensor([0, 8192, 11192, 11892], dtype=torch.int32, device=DEV)
+    fo, flse, _, _ = _flash_attn_varlen_forward(q, k, v, cu, cu, 8192, 8192, 0.0, 128 ** -0.5, True)
+    out, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, DEV), 128 ** -0.5)
+    torch.testing.assert_close(out.float(), fo.float(), rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(lse, flse, rtol=1e-3, atol=3e-3)
