@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--cost", default="b200", choices=["b200", "flops"],
                     help="LB cost beta/alpha: FLOP ratio ('flops') or FLOP ratio x measured kernel-throughput ratio")
     ap.add_argument("--attn", default="tcgen05", choices=["tcgen05", "flash"],
-                    help="attention forward kernel (backward is flash-attn either way)")
+                    help="attention kernels: own tcgen05 fwd+bwd, or flash-attn 2.8 (library)")
     ap.add_argument("--cache-params", action="store_true",
                     help="SURVEY 8(f)1: keep fetched units for the whole minibatch (one fetch per unit per step)")
     ap.add_argument("--model", default="qwen2.5-1.5b")
@@ -308,7 +308,7 @@ def run_sft(args):
                 if not mb:
                     worker.empty_microbatch()
                     continue
-                b = batches[j] if batches is not None else W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads)
+                b = batches[j] if batches is not None else W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads, kv_heads=shape.kv_heads)
                 ntok = sum(lens[i] for i in mb)
                 loss += worker.microbatch(b, ntok / total) * (ntok / total)
             t1.record(stream)
@@ -323,7 +323,7 @@ def run_sft(args):
         pre = {}
         if resident:
             for k in timed_steps:
-                pre[k] = [W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads) if mb else None
+                pre[k] = [W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads, kv_heads=shape.kv_heads) if mb else None
                           for mb in plan[k % len(plan)][rank]]
         torch.cuda.synchronize()
         if world > 1:
@@ -382,7 +382,7 @@ def run_sft(args):
                 "launches": gm["launches"], "ms_per_launch": round(gm["ms"] / gm["launches"], 4),
                 "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": None}
     pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
-    h2d = sum(16 * lens[i] + 8 + 16 * shape.heads * ((lens[i] + 127) // 128)  # ids, labels, positions, cu, attn items
+    h2d = sum(16 * lens[i] + 8 + 16 * (shape.heads + shape.kv_heads) * ((lens[i] + 127) // 128)  # + attn work lists
               for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -397,7 +397,7 @@ def run_sft(args):
                            "lengths": "lognormal(8,1.5) n=2048 cap=32768 seed=0, floor 512",
                            "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
                            "cost_beta_over_alpha": round(beta, 1), "cost_model": args.cost,
-                           "cache_params": args.cache_params, "attention_fwd": args.attn,
+                           "cache_params": args.cache_params, "attention": args.attn,
                            "tokens_timed": res["tokens"], "l2": "inputs > L2 (GBs of activations/units), no flush"},
                 "idle_fraction": round(res["idle"], 4),
                 "idle_note": "1 - sum(busy)/(N*T), busy = device time from step start to the minibatch barrier",
@@ -475,7 +475,7 @@ def write_trace(path, shape, comm, plan, lens, k, rank, world, dev):
     total = float(sum(lens[i] for dv in plan[k % len(plan)] for mb in dv for i in mb))
     for mb in plan[k % len(plan)][rank]:
         ntok = sum(lens[i] for i in mb)
-        worker.microbatch(W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads), ntok / total)
+        worker.microbatch(W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads, kv_heads=shape.kv_heads), ntok / total)
     worker.tracer.span("barrier", 0, cur, False)
     row = worker.tracer.rows[-1]
     worker.minibatch_end()

@@ -76,6 +76,10 @@ __host__ __device__ constexpr unsigned idesc(int b_mn_major) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(b_mn_major) << 16) | ((128u >> 3) << 17) |
            ((128u >> 4) << 24);
 }
+__host__ __device__ constexpr unsigned instr(int a_mn_major, int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(a_mn_major) << 15) |
+           (static_cast<unsigned>(b_mn_major) << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+}
 __device__ __forceinline__ void mma(unsigned d, std::uint64_t a, std::uint64_t b, unsigned id, unsigned acc) {
     asm volatile(
         "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
@@ -334,6 +338,270 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ======================================================================
+// Backward. One CTA per (sequence, 128-key tile j, kv head): K_j and V_j stay
+// in smem, dK_j / dV_j accumulate in TMEM over every query head of the GQA
+// group and every query tile i >= j (causal), so they are written once, with
+// no atomics. Per (head, i):
+//   MMA  S = Q_i K_j^T, dP = dO_i V_j^T                      (TMEM S, dP)
+//   SM   P = exp(scale*S - lse), dS = scale * P * (dP - D)    (bf16 -> smem)
+//   MMA  dV += P^T dO_i, dK += dS^T Q_i  (A operands MN-major: P / dS stored
+//        [q][key] are read transposed in place), dQ_i = dS K_j (into S's cols)
+//   SM   dQ_i rows -> red.global.add.v4.f32 into the fp32 dQ accumulator
+// D = rowsum(dO * O) comes from attn_bwd_prep_kernel; dq_convert makes bf16.
+// TMEM: dV [0,128) dK [128,256) S/dQ [256,384) dP [384,512).
+struct BwdArgs {
+    const Item* items;  // {seq_start, seq_len, kv_tile, kv_head}
+    int H, KV;
+    float scale, scale_log2;
+    const float* lse;  // [H][T]
+    const float* D;    // [H][T]
+    float* dq_acc;     // [T][H][HD] fp32
+    __nv_bfloat16* dk;  // [T][KV][HD]
+    __nv_bfloat16* dv;
+    long long T;
+};
+
+__device__ __forceinline__ void store_swizzled(char* tile, int r, int c, const unsigned* pk) {
+    // 32 bf16 of row r, columns [c, c+32) of a [128][128] K-major SW128 tile (two 64-column halves)
+    char* half = tile + (c >> 6) * (kTile / 2) + r * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int chunk = ((c & 63) >> 3) + q;
+        *reinterpret_cast<uint4*>(half + ((chunk ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do, BwdArgs g) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    char* sK = smem;
+    char* sV = smem + kTile;
+    char* sQ = smem + 2 * kTile;
+    char* sdO = smem + 3 * kTile;
+    char* sP = smem + 4 * kTile;
+    char* sdS = smem + 5 * kTile;
+    __shared__ __align__(8) unsigned long long kv_full, qdo_full, qdo_empty, s_full, ds_full, dq_full, s_free;
+    __shared__ unsigned tmem_base;
+
+    const Item it = g.items[blockIdx.x];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int j = it.q_tile;  // key tile
+    const int kvh = it.head;
+    const int G = g.H / g.KV;
+    const int n_q = (it.seq_len + BQ - 1) / BQ;
+    const int per_head = n_q - j;  // query tiles i = j .. n_q-1
+    const int n_iter = G * per_head;
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(&kv_full, 1);
+        mbar_init(&qdo_full, 1);
+        mbar_init(&qdo_empty, 1);
+        mbar_init(&s_full, 1);
+        mbar_init(&ds_full, 4);
+        mbar_init(&dq_full, 1);
+        mbar_init(&s_free, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base;
+    const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA
+            const int k0 = it.seq_start + j * BKV;
+            mbar_expect_tx(&kv_full, 2 * kTile);
+            tma_2d(&map_k, &kv_full, sK, kvh * HD, k0);
+            tma_2d(&map_k, &kv_full, sK + kTile / 2, kvh * HD + 64, k0);
+            tma_2d(&map_v, &kv_full, sV, kvh * HD, k0);
+            tma_2d(&map_v, &kv_full, sV + kTile / 2, kvh * HD + 64, k0);
+            for (int n = 0; n < n_iter; ++n) {
+                const int h = kvh * G + n / per_head, i = j + n % per_head;
+                if (n > 0) mbar_wait(&qdo_empty, (n - 1) & 1);
+                const int q0 = it.seq_start + i * BQ;
+                mbar_expect_tx(&qdo_full, 2 * kTile);
+                tma_2d(&map_q, &qdo_full, sQ, h * HD, q0);
+                tma_2d(&map_q, &qdo_full, sQ + kTile / 2, h * HD + 64, q0);
+                tma_2d(&map_do, &qdo_full, sdO, h * HD, q0);
+                tma_2d(&map_do, &qdo_full, sdO + kTile / 2, h * HD + 64, q0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const unsigned id_kk = instr(0, 0), id_mm = instr(1, 1), id_km = instr(0, 1);
+            mbar_wait(&kv_full, 0);
+            const unsigned qa = su32(sQ), doa = su32(sdO), ka = su32(sK), va = su32(sV), pa = su32(sP),
+                           dsa = su32(sdS);
+            for (int n = 0; n < n_iter; ++n) {
+                mbar_wait(&qdo_full, n & 1);
+                if (n > 0) mbar_wait(&s_free, (n - 1) & 1);  // dQ_{n-1} read out of the S columns
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {  // K = head dim, K-major halves
+                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + T_S, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_kk, kk > 0);
+                    mma(tmem + T_DP, sdesc(doa + off, 16, 1024), sdesc(va + off, 16, 1024), id_kk, kk > 0);
+                }
+                commit(&s_full);
+                mbar_wait(&ds_full, n & 1);  // P, dS in smem
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk) {  // K = query rows: MN-major A (P^T, dS^T) and B (dO, Q)
+                    const unsigned off = kk * 2048;
+                    mma(tmem + T_DV, sdesc(pa + off, kTile / 2, 1024), sdesc(doa + off, kTile / 2, 1024), id_mm,
+                        (n > 0 || kk > 0));
+                    mma(tmem + T_DK, sdesc(dsa + off, kTile / 2, 1024), sdesc(qa + off, kTile / 2, 1024), id_mm,
+                        (n > 0 || kk > 0));
+                }
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K: A K-major (by key), B = K MN-major
+                    const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + T_S, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
+                }
+                commit(&qdo_empty);  // Q_i, dO_i (and P, dS) consumed
+                commit(&dq_full);
+            }
+        }
+    } else {  // ---- softmax-gradient / dQ / dK dV epilogue (warps 2..5)
+        const int quad = warp % 4;
+        const int r = quad * 32 + lane;  // row: query within tile i (loop) / key within tile j (epilogue)
+        const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
+        for (int n = 0; n < n_iter; ++n) {
+            const int h = kvh * G + n / per_head, i = j + n % per_head;
+            const int qi = i * BQ + r;  // query index within the sequence
+            const bool q_ok = qi < it.seq_len;
+            const long long tok = static_cast<long long>(it.seq_start) + qi;
+            const float lse2 = q_ok ? g.lse[static_cast<long long>(h) * g.T + tok] * kLog2e : 0.f;
+            const float Dr = q_ok ? g.D[static_cast<long long>(h) * g.T + tok] : 0.f;
+            // keys e of tile j visible to query qi
+            const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV : -1;
+            mbar_wait(&s_full, n & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c = 0; c < BKV; c += 32) {
+                unsigned sv[32], dp[32];
+                TM_LD32(tmem + lane_base + T_S + c, sv);
+                TM_LD32(tmem + lane_base + T_DP + c, dp);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                unsigned pk[16], dk2[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    float p0 = ex2(__uint_as_float(sv[e]) * g.scale_log2 - lse2);
+                    float p1 = ex2(__uint_as_float(sv[e + 1]) * g.scale_log2 - lse2);
+                    if (c + e > lim) p0 = 0.f;
+                    if (c + e + 1 > lim) p1 = 0.f;
+                    const float d0 = g.scale * p0 * (__uint_as_float(dp[e]) - Dr);
+                    const float d1 = g.scale * p1 * (__uint_as_float(dp[e + 1]) - Dr);
+                    __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
+                    pk[e / 2] = *reinterpret_cast<unsigned*>(&hp);
+                    dk2[e / 2] = *reinterpret_cast<unsigned*>(&hd);
+                }
+                store_swizzled(sP, r, c, pk);
+                store_swizzled(sdS, r, c, dk2);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ds_full);
+            // dQ_i (fp32, already scaled) -> global accumulator
+            mbar_wait(&dq_full, n & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float* dqrow = g.dq_acc + (tok * g.H + h) * HD;
+#pragma unroll 1
+            for (int c = 0; c < HD; c += 32) {
+                unsigned v[32];
+                TM_LD32(tmem + lane_base + T_S + c, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (q_ok) {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 4)
+                        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c + e),
+                                     "f"(__uint_as_float(v[e])), "f"(__uint_as_float(v[e + 1])),
+                                     "f"(__uint_as_float(v[e + 2])), "f"(__uint_as_float(v[e + 3]))
+                                     : "memory");
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free);
+        }
+        // dK, dV of the key tile (complete: the last dq_full covers every MMA)
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int kj = j * BKV + r;
+        const bool k_ok = kj < it.seq_len;
+        const long long ktok = static_cast<long long>(it.seq_start) + kj;
+        for (int which = 0; which < 2; ++which) {
+            __nv_bfloat16* dst = (which ? g.dk : g.dv) + (ktok * g.KV + kvh) * HD;
+            const unsigned col = which ? T_DK : T_DV;
+#pragma unroll 1
+            for (int c = 0; c < HD; c += 32) {
+                unsigned v[32];
+                TM_LD32(tmem + lane_base + col + c, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (k_ok) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 o;
+                        unsigned* w = reinterpret_cast<unsigned*>(&o);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(v[8 * q + 2 * e]),
+                                                                      __uint_as_float(v[8 * q + 2 * e + 1]));
+                            w[e] = *reinterpret_cast<unsigned*>(&hh);
+                        }
+                        *reinterpret_cast<uint4*>(dst + c + 8 * q) = o;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// D[h][t] = sum_c dO[t][h][c] * O[t][h][c]; one warp per (t, h) row; also zeroes dq_acc rows
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                     float* __restrict__ D, float* __restrict__ dq_acc, long long T, int H) {
+    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (row >= T * H) return;
+    const uint2 a = reinterpret_cast<const uint2*>(o + row * HD)[lane];
+    const uint2 b = reinterpret_cast<const uint2*>(dout + row * HD)[lane];
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+    float acc = __low2float(a2[0]) * __low2float(b2[0]) + __high2float(a2[0]) * __high2float(b2[0]) +
+                __low2float(a2[1]) * __low2float(b2[1]) + __high2float(a2[1]) * __high2float(b2[1]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    const long long t = row / H;
+    const int h = static_cast<int>(row % H);
+    if (lane == 0) D[static_cast<long long>(h) * T + t] = acc;
+    reinterpret_cast<float4*>(dq_acc + row * HD)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void dq_convert_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, long long n4) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float4 v = acc[i];
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+        dq[i] = make_uint2(*reinterpret_cast<unsigned*>(&a), *reinterpret_cast<unsigned*>(&b));
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -401,5 +669,59 @@ extern "C" odc_status odc_attn_fwd(const void* q, const void* k, const void* v, 
         attn_fwd_kernel<<<n_items, kThreads, kSmem, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, a);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw std::runtime_error(std::string("attn_fwd launch: ") + cudaGetErrorString(e));
+    });
+}
+
+extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                   const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                                   const void* items, int n_items, std::int64_t T, int H, int KV, int head_dim,
+                                   float scale, void* stream) {
+    return odc::guard([&] {
+        using namespace odc::attn;
+        if (head_dim != HD) throw odcsim::ParamError("attn_bwd: head_dim must be 128");
+        if (KV < 1 || H % KV) throw odcsim::ParamError("attn_bwd: H must be a multiple of KV");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        static thread_local int configured = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (configured != dev) {
+            cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
+            configured = dev;
+        }
+        // workspace: D [H][T] fp32, then dq_acc [T][H][HD] fp32
+        float* D = static_cast<float*>(workspace);
+        float* dq_acc = D + (static_cast<long long>(H) * T + 63) / 64 * 64;  // keep the accumulator 256B-aligned
+        const long long rows = T * H;
+        odc::count_launch();
+        attn_bwd_prep_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), D, dq_acc, T, H);
+        // zero dK / dV rows no key tile writes (tokens past every sequence end never exist here; all rows covered)
+        if (n_items > 0) {
+            CUtensorMap mq = rows_map(q, static_cast<long long>(H) * HD, T);
+            CUtensorMap mk = rows_map(k, static_cast<long long>(KV) * HD, T);
+            CUtensorMap mv = rows_map(v, static_cast<long long>(KV) * HD, T);
+            CUtensorMap mdo = rows_map(dout, static_cast<long long>(H) * HD, T);
+            BwdArgs a{};
+            a.items = static_cast<const Item*>(items);
+            a.H = H;
+            a.KV = KV;
+            a.scale = scale;
+            a.scale_log2 = scale * kLog2e;
+            a.lse = lse;
+            a.D = D;
+            a.dq_acc = dq_acc;
+            a.dk = static_cast<__nv_bfloat16*>(dk);
+            a.dv = static_cast<__nv_bfloat16*>(dv);
+            a.T = T;
+            odc::count_launch();
+            attn_bwd_kernel<<<n_items, kThreads, kSmem, st>>>(mq, mk, mv, mdo, a);
+        }
+        odc::count_launch();
+        const long long n4 = rows * HD / 4;
+        dq_convert_kernel<<<static_cast<unsigned>(std::min<long long>((n4 + 255) / 256, 148 * 8)), 256, 0, st>>>(
+            reinterpret_cast<const float4*>(dq_acc), static_cast<uint2*>(dq), n4);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw std::runtime_error(std::string("attn_bwd launch: ") + cudaGetErrorString(e));
     });
 }

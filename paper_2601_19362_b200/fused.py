@@ -103,3 +103,29 @@ def attn_fwd(q, k, v, items, scale):
     check(lib().odc_attn_fwd(_p(q), _p(k), _p(v), _p(out), _p(lse), _p(items), items.shape[0], T, H, KV, hd,
                              float(scale), _s()))
     return out, lse
+
+
+def attn_bwd_items(lens, KV: int, device) -> torch.Tensor:
+    """Backward work list: one item per (sequence, 128-key tile, kv head),
+    most query tiles (causal) first."""
+    items, start = [], 0
+    for n in lens:
+        nt = (n + 127) // 128
+        for kt in range(nt):
+            for h in range(KV):
+                items.append((start, n, kt, h, nt - kt))
+        start += n
+    items.sort(key=lambda t: -t[4])
+    return torch.tensor([t[:4] for t in items], dtype=torch.int32).to(device, non_blocking=True)
+
+
+def attn_bwd(q, k, v, o, dout, lse, items, scale):
+    T, H, hd = q.shape
+    KV = k.shape[1]
+    dq = torch.empty_like(q)
+    dk = torch.empty_like(k)
+    dv = torch.empty_like(v)
+    ws = torch.empty((H * T + 63) // 64 * 64 + T * H * hd, dtype=torch.float32, device=q.device)
+    check(lib().odc_attn_bwd(_p(q), _p(k), _p(v), _p(o), _p(dout), _p(lse), _p(dq), _p(dk), _p(dv), _p(ws),
+                             _p(items), items.shape[0], T, H, KV, hd, float(scale), _s()))
+    return dq, dk, dv

@@ -234,10 +234,12 @@ class Batch:
     cu_seqlens: torch.Tensor  # [n+1] int32
     max_len: int
     tokens: int
-    attn_items: Optional[torch.Tensor] = None  # tcgen05 attention work list (built per microbatch)
+    attn_items: Optional[torch.Tensor] = None  # tcgen05 attention work lists (built per microbatch)
+    attn_bwd_items: Optional[torch.Tensor] = None
 
 
-def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, device, heads: int = 0) -> Batch:
+def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, device, heads: int = 0,
+               kv_heads: int = 0) -> Batch:
     """Synthetic packed microbatch: token ids seeded by the global sample id, so
     every implementation sees identical data."""
     ids, labels, pos, cu = [], [], [], [0]
@@ -257,12 +259,14 @@ def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, devic
               torch.tensor(cu, dtype=torch.int32).to(device, non_blocking=True),
               max(int(lens[s]) for s in sample_ids), T)
     if heads:
-        attach_attn_items(b, [int(lens[s]) for s in sample_ids], heads, device)
+        attach_attn_items(b, [int(lens[s]) for s in sample_ids], heads, device, kv_heads)
     return b
 
 
-def attach_attn_items(b: Batch, seq_lens: Sequence[int], heads: int, device) -> Batch:
+def attach_attn_items(b: Batch, seq_lens: Sequence[int], heads: int, device, kv_heads: int = 0) -> Batch:
     b.attn_items = F.attn_items(list(seq_lens), heads, device)
+    if kv_heads:
+        b.attn_bwd_items = F.attn_bwd_items(list(seq_lens), kv_heads, device)
     return b
 
 
@@ -283,7 +287,7 @@ class Worker:
         self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
         self.rope = F.rope_table(max_positions, shape.head_dim, ROPE_THETA, self.dev)
         self.tracer: Optional[Tracer] = None
-        # attention forward: own tcgen05 kernel (csrc/attention.cu) or flash-attn; backward: flash-attn
+        # attention: own tcgen05 kernels (csrc/attention.cu) or flash-attn 2.8 (library) for both passes
         self.attn = attn if shape.head_dim == 128 else "flash"
         # parameters cannot change inside a minibatch, so with
         # HBM to spare every unit is fetched once per minibatch and reused by
@@ -327,9 +331,9 @@ class Worker:
         scale = 1.0 / math.sqrt(hd)
         lay = layer_layout(s)
         tab = self.rope
-        if self.attn == "tcgen05" and b.attn_items is None:
+        if self.attn == "tcgen05" and (b.attn_items is None or b.attn_bwd_items is None):
             cu = b.cu_seqlens.tolist()
-            attach_attn_items(b, [cu[i + 1] - cu[i] for i in range(len(cu) - 1)], H, self.dev)
+            attach_attn_items(b, [cu[i + 1] - cu[i] for i in range(len(cu) - 1)], H, self.dev, KV)
 
         # ---------------- forward
         ev_e = self._fetch_unit(0, after=_record(cur))
@@ -416,11 +420,15 @@ class Worker:
             # attention block
             do = G.linear_dgrad(dhm, P["o_w"])
             G.linear_wgrad(dhm, o.view(T, -1), out=Gv["o_w"])
-            dq = torch.empty_like(q)
-            dk = torch.empty_like(k)
-            dv = torch.empty_like(v)
-            _flash_attn_varlen_backward(do.view(T, H, hd), q, k, v, o, lse, dq, dk, dv, b.cu_seqlens, b.cu_seqlens,
-                                        b.max_len, b.max_len, 0.0, scale, True, -1, -1, 0.0, None, False)
+            if self.attn == "tcgen05":
+                dq, dk, dv = F.attn_bwd(q, k, v, o, do.view(T, H, hd), lse, b.attn_bwd_items, scale)
+            else:
+                dq = torch.empty_like(q)
+                dk = torch.empty_like(k)
+                dv = torch.empty_like(v)
+                _flash_attn_varlen_backward(do.view(T, H, hd), q, k, v, o, lse, dq, dk, dv, b.cu_seqlens,
+                                            b.cu_seqlens, b.max_len, b.max_len, 0.0, scale, True, -1, -1, 0.0, None,
+                                            False)
             dqkv = F.qkv_rope_bwd(dq, dk, dv, tab, b.positions, H, KV, hd)
             del dq, dk, dv, do
             if "qkv_b" in Gv:

@@ -56,3 +56,24 @@ def test_attn_fwd_matches_flash_attn_long():
     out, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, DEV), 128 ** -0.5)
     torch.testing.assert_close(out.float(), fo.float(), rtol=2e-2, atol=2e-2)
     torch.testing.assert_close(lse, flse, rtol=1e-3, atol=3e-3)
+
+
+@pytest.mark.parametrize("lens,H,KV", [([128], 2, 1), ([300, 77, 513], 12, 2), ([1000, 2048], 4, 2),
+                                       ([129, 255, 256, 257], 6, 3), ([1], 2, 2)])
+def test_attn_bwd_matches_reference(lens, H, KV):
+    torch.manual_seed(2)
+    T = sum(lens)
+    q = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
+    k = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    v = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    do = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
+    scale = 128 ** -0.5
+    out, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, DEV), scale)
+    dq, dk, dv = F.attn_bwd(q, k, v, out, do, lse, F.attn_bwd_items(lens, KV, DEV), scale)
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    ro, _ = _ref(qf, kf, vf, lens, scale)
+    ro.backward(do.float())
+    for got, want in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
+        rel = ((got.float() - want).norm() / want.norm().clamp_min(1e-6)).item()
+        assert rel < 2e-2 or want.norm() < 1e-4, rel
+        torch.testing.assert_close(got.float(), want, rtol=5e-2, atol=5e-2)
