@@ -43,16 +43,16 @@ class Shape:
 
     def beta_over_alpha_b200(self) -> float:
         """FLOP ratio scaled by the measured B200 throughput ratio of the two
-        terms' kernels: flash-attn varlen fwd+bwd ~330 TFLOP/s
-        (profiles/r01 attention probe) vs the tcgen05 GEMMs ~1,270 TFLOP/s in
-        the step, i.e. an attention FLOP costs ~3.85x a dense FLOP. The cost
+        terms' kernels: the tcgen05 attention fwd+bwd ~500 TFLOP/s (fwd
+        500-755, bwd 437-513, profiles/r01) vs the tcgen05 GEMMs ~1,280
+        TFLOP/s in the step, i.e. an attention FLOP costs ~2.6x a dense FLOP. The cost
         model's absolute scale is a free knob (inc/cost_model.hpp:10-12); only
         beta/alpha shapes the plan, identically for ODC and FSDP."""
         return self.beta_over_alpha() * (ATTN_TFLOPS / GEMM_TFLOPS)
 
 
-ATTN_TFLOPS = 330.0
-GEMM_TFLOPS = 1270.0
+ATTN_TFLOPS = 500.0
+GEMM_TFLOPS = 1280.0
 
 QWEN25_1_5B = Shape("qwen2.5-1.5b", 1536, 8960, 28, 12, 2, 151936, True, True)
 LLAMA3_8B = Shape("llama-3-8b", 4096, 14336, 32, 32, 8, 128256, False, False)
