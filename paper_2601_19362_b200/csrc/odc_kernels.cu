@@ -187,13 +187,17 @@ cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s) {
 // ---------------------------------------------------- fetch (TMA bulk)
 // The fetch engine proper. One elected thread per CTA streams chunks
 // peer HBM --cp.async.bulk--> smem --cp.async.bulk--> local HBM through a
-// kTmaStages-deep mbarrier pipeline, so each CTA keeps ~96 KB of NVLink reads
+// kTmaStages-deep mbarrier pipeline, so each CTA keeps kTmaSmem of NVLink reads
 // in flight from a single thread; a small CTA budget leaves the SMs to the
 // model's kernels. Every CTA owns a contiguous slice of EVERY owner's shard
 // and walks the slices round-robin, so all owners (and the local shard) are
 // served concurrently instead of one after the other. Bytes before the first
 // 16-byte-aligned address and after the last one (ragged shards) are moved
 // by a second warp.
+// 4 x 32 KB per CTA: ~128 KB of NVLink reads in flight per CTA is what the
+// link needs (64 CTAs: 645 GB/s at N=2). A 3 x 8 KB variant that fits next to
+// a resident GEMM/attention CTA reached only 340 GB/s and did not change the
+// SFT step (profiles/r01/p2p_n2_smallsmem.md), so the big ring stays.
 constexpr int kTmaChunk = 32768;
 constexpr int kTmaStages = 4;
 constexpr int kTmaThreads = 64;

@@ -48,7 +48,9 @@ class Shape:
         TFLOP/s in the step, i.e. an attention FLOP costs ~2.6x a dense FLOP. The cost
         model's absolute scale is a free knob (inc/cost_model.hpp:10-12); only
         beta/alpha shapes the plan, identically for ODC and FSDP."""
-        return self.beta_over_alpha() * (ATTN_TFLOPS / GEMM_TFLOPS)
+        # the LM head (6*V*d per token, tcgen05 GEMM) is linear work too
+        linear = (self.nonembed_params + self.vocab * self.d) / (self.layers * self.d)
+        return linear * (ATTN_TFLOPS / GEMM_TFLOPS)
 
 
 ATTN_TFLOPS = 500.0
