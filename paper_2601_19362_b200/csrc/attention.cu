@@ -346,10 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   MMA  S = Q_i K_j^T, dP = dO_i V_j^T                      (TMEM S, dP)
 //   SM   P = exp(scale*S - lse), dS = scale * P * (dP - D)    (bf16 -> smem)
 //   MMA  dV += P^T dO_i, dK += dS^T Q_i  (A operands MN-major: P / dS stored
-//        [q][key] are read transposed in place), dQ_i = dS K_j (into S's cols)
-//   SM   dQ_i rows -> red.global.add.v4.f32 into the fp32 dQ accumulator
+//        [q][key] are read transposed in place), dQ_i = dS K_j (into dP's cols)
+//   SM   dQ_i rows -> red.global.add.v4.f32 into the fp32 dQ accumulator,
+//        overlapping the next S = Q K^T (dP waits for the read-out)
 // D = rowsum(dO * O) comes from attn_bwd_prep_kernel; dq_convert makes bf16.
-// TMEM: dV [0,128) dK [128,256) S/dQ [256,384) dP [384,512).
+// TMEM: dV [0,128) dK [128,256) S [256,384) dP/dQ [384,512).
 struct BwdArgs {
     const Item* items;  // {seq_start, seq_len, kv_tile, kv_head}
     int H, KV;
@@ -384,7 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     char* sdO = smem + 3 * kTile;
     char* sP = smem + 4 * kTile;
     char* sdS = smem + 5 * kTile;
-    __shared__ __align__(8) unsigned long long kv_full, qdo_full, qdo_empty, s_full, ds_full, dq_full, s_free;
+    // sdp_full: S_n and dP_n in TMEM; ds_full: P_n / dS_n in smem (S_n, dP_n consumed);
+    // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
+    __shared__ __align__(8) unsigned long long kv_full, qdo_full, qdo_empty, sdp_full, ds_full, dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
     const Item it = g.items[blockIdx.x];
@@ -400,10 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&kv_full, 1);
         mbar_init(&qdo_full, 1);
         mbar_init(&qdo_empty, 1);
-        mbar_init(&s_full, 1);
+        mbar_init(&sdp_full, 1);
         mbar_init(&ds_full, 4);
         mbar_init(&dq_full, 1);
-        mbar_init(&s_free, 4);
+        mbar_init(&dq_read, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const unsigned tmem = tmem_base;
-    const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;
+    const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;  // dQ_n reuses T_DP
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA
@@ -444,16 +447,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                            dsa = su32(sdS);
             for (int n = 0; n < n_iter; ++n) {
                 mbar_wait(&qdo_full, n & 1);
-                if (n > 0) mbar_wait(&s_free, (n - 1) & 1);  // dQ_{n-1} read out of the S columns
+                // S columns were consumed by softmax(n-1) before its ds_full (waited below at n-1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {  // K = head dim, K-major halves
+                for (int kk = 0; kk < HD / 16; ++kk) {  // S = Q K^T (overlaps the dQ_{n-1} read-out)
                     const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_S, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_kk, kk > 0);
+                }
+                if (n > 0) mbar_wait(&dq_read, (n - 1) & 1);  // dP columns free again
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {  // dP = dO V^T
+                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_DP, sdesc(doa + off, 16, 1024), sdesc(va + off, 16, 1024), id_kk, kk > 0);
                 }
-                commit(&s_full);
-                mbar_wait(&ds_full, n & 1);  // P, dS in smem
+                commit(&sdp_full);
+                mbar_wait(&ds_full, n & 1);  // P, dS in smem; S, dP read
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk) {  // K = query rows: MN-major A (P^T, dS^T) and B (dO, Q)
@@ -464,11 +473,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         (n > 0 || kk > 0));
                 }
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K: A K-major (by key), B = K MN-major
+                for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
                     const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                    mma(tmem + T_S, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
+                    mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
                 }
-                commit(&qdo_empty);  // Q_i, dO_i (and P, dS) consumed
+                commit(&qdo_empty);  // Q_n, dO_n (and P, dS) consumed
                 commit(&dq_full);
             }
         }
@@ -483,48 +492,54 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long tok = static_cast<long long>(it.seq_start) + qi;
             const float lse2 = q_ok ? g.lse[static_cast<long long>(h) * g.T + tok] * kLog2e : 0.f;
             const float Dr = q_ok ? g.D[static_cast<long long>(h) * g.T + tok] : 0.f;
-            // keys e of tile j visible to query qi
-            const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV : -1;
-            mbar_wait(&s_full, n & 1);
+            const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV : -1;  // visible keys of tile j
+            mbar_wait(&sdp_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-            for (int c = 0; c < BKV; c += 32) {
-                unsigned sv[32], dp[32];
+            for (int c = 0; c < BKV; c += 64) {  // 64-column halves: 4 TMEM loads, one wait
+                unsigned sv[64], dp[64];
                 TM_LD32(tmem + lane_base + T_S + c, sv);
+                TM_LD32(tmem + lane_base + T_S + c + 32, (sv + 32));
                 TM_LD32(tmem + lane_base + T_DP + c, dp);
+                TM_LD32(tmem + lane_base + T_DP + c + 32, (dp + 32));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                unsigned pk[16], dk2[16];
 #pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    float p0 = ex2(__uint_as_float(sv[e]) * g.scale_log2 - lse2);
-                    float p1 = ex2(__uint_as_float(sv[e + 1]) * g.scale_log2 - lse2);
-                    if (c + e > lim) p0 = 0.f;
-                    if (c + e + 1 > lim) p1 = 0.f;
-                    const float d0 = g.scale * p0 * (__uint_as_float(dp[e]) - Dr);
-                    const float d1 = g.scale * p1 * (__uint_as_float(dp[e + 1]) - Dr);
-                    __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
-                    pk[e / 2] = *reinterpret_cast<unsigned*>(&hp);
-                    dk2[e / 2] = *reinterpret_cast<unsigned*>(&hd);
+                for (int half = 0; half < 64; half += 32) {
+                    unsigned pk[16], dk2[16];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const int x = half + e;
+                        float p0 = ex2(__uint_as_float(sv[x]) * g.scale_log2 - lse2);
+                        float p1 = ex2(__uint_as_float(sv[x + 1]) * g.scale_log2 - lse2);
+                        if (c + x > lim) p0 = 0.f;
+                        if (c + x + 1 > lim) p1 = 0.f;
+                        const float d0 = g.scale * p0 * (__uint_as_float(dp[x]) - Dr);
+                        const float d1 = g.scale * p1 * (__uint_as_float(dp[x + 1]) - Dr);
+                        __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
+                        pk[e / 2] = *reinterpret_cast<unsigned*>(&hp);
+                        dk2[e / 2] = *reinterpret_cast<unsigned*>(&hd);
+                    }
+                    store_swizzled(sP, r, c + half, pk);
+                    store_swizzled(sdS, r, c + half, dk2);
                 }
-                store_swizzled(sP, r, c, pk);
-                store_swizzled(sdS, r, c, dk2);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&ds_full);
-            // dQ_i (fp32, already scaled) -> global accumulator
+            // dQ_n (fp32, already scaled) -> global accumulator, while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float* dqrow = g.dq_acc + (tok * g.H + h) * HD;
 #pragma unroll 1
-            for (int c = 0; c < HD; c += 32) {
-                unsigned v[32];
-                TM_LD32(tmem + lane_base + T_S + c, v);
+            for (int c = 0; c < HD; c += 64) {
+                unsigned v[64];
+                TM_LD32(tmem + lane_base + T_DP + c, v);
+                TM_LD32(tmem + lane_base + T_DP + c + 32, (v + 32));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (q_ok) {
 #pragma unroll
-                    for (int e = 0; e < 32; e += 4)
+                    for (int e = 0; e < 64; e += 4)
                         asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c + e),
                                      "f"(__uint_as_float(v[e])), "f"(__uint_as_float(v[e + 1])),
                                      "f"(__uint_as_float(v[e + 2])), "f"(__uint_as_float(v[e + 3]))
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_free);
+            if (lane == 0) mbar_arrive(&dq_read);
         }
         // dK, dV of the key tile (complete: the last dq_full covers every MMA)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
