@@ -208,8 +208,9 @@ odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, i
 odc_status odc_attn_fwd(const void* q, const void* k, const void* v, void* out, float* lse, const void* items,
                         int n_items, int64_t T, int H, int KV, int head_dim, float scale, void* stream);
 /* Backward: dq [T][H][128], dk / dv [T][KV][128] bf16 from q, k, v, o, dout and the forward's lse.
- * items: {seq_start, seq_len, kv_tile, kv_head} (one CTA each, heaviest first);
- * workspace: fp32, roundup(H*T, 64) + T*H*128 elements, 16-byte aligned. */
+ * items: int32 x8 {seq_start, seq_len, kv_tile, kv_head, it_begin, it_end, 0, 0} (one CTA each,
+ * heaviest first; iterations n in [it_begin, it_end) of (head-in-group = n / tiles, q tile = kv_tile + n % tiles));
+ * workspace: fp32, roundup(H*T, 64) + T*H*128 + 2*T*KV*128 elements, 16-byte aligned. */
 odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
                         const float* lse, void* dq, void* dk, void* dv, void* workspace, const void* items,
                         int n_items, int64_t T, int H, int KV, int head_dim, float scale, void* stream);

@@ -351,15 +351,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 //        overlapping the next S = Q K^T (dP waits for the read-out)
 // D = rowsum(dO * O) comes from attn_bwd_prep_kernel; dq_convert makes bf16.
 // TMEM: dV [0,128) dK [128,256) S [256,384) dP/dQ [384,512).
+// A backward work item: key tile kv_tile of one sequence for one kv head,
+// iterations [it_begin, it_end) of the (query head of the group, query tile
+// i >= kv_tile) loop. Long causal loops are split into several items so the
+// grid load-balances; their dK / dV partials meet in fp32 accumulators.
+struct BwdItem {
+    int seq_start, seq_len, kv_tile, kv_head, it_begin, it_end, pad0, pad1;
+};
+
 struct BwdArgs {
-    const Item* items;  // {seq_start, seq_len, kv_tile, kv_head}
+    const BwdItem* items;
     int H, KV;
     float scale, scale_log2;
     const float* lse;  // [H][T]
     const float* D;    // [H][T]
     float* dq_acc;     // [T][H][HD] fp32
-    __nv_bfloat16* dk;  // [T][KV][HD]
-    __nv_bfloat16* dv;
+    float* dk_acc;     // [T][KV][HD] fp32
+    float* dv_acc;
     long long T;
 };
 
@@ -390,14 +398,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ __align__(8) unsigned long long kv_full, qdo_full, qdo_empty, sdp_full, ds_full, dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
-    const Item it = g.items[blockIdx.x];
+    const BwdItem it = g.items[blockIdx.x];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int j = it.q_tile;  // key tile
-    const int kvh = it.head;
+    const int j = it.kv_tile;  // key tile
+    const int kvh = it.kv_head;
     const int G = g.H / g.KV;
     const int n_q = (it.seq_len + BQ - 1) / BQ;
-    const int per_head = n_q - j;  // query tiles i = j .. n_q-1
-    const int n_iter = G * per_head;
+    const int per_head = n_q - j;  // query tiles i = j .. n_q-1 for each head of the group
+    const int n0 = it.it_begin;
+    const int n_iter = it.it_end - it.it_begin;
 
     if (warp == 0 && lane == 0) {
         mbar_init(&kv_full, 1);
@@ -429,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_2d(&map_v, &kv_full, sV, kvh * HD, k0);
             tma_2d(&map_v, &kv_full, sV + kTile / 2, kvh * HD + 64, k0);
             for (int n = 0; n < n_iter; ++n) {
-                const int h = kvh * G + n / per_head, i = j + n % per_head;
+                const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
                 if (n > 0) mbar_wait(&qdo_empty, (n - 1) & 1);
                 const int q0 = it.seq_start + i * BQ;
                 mbar_expect_tx(&qdo_full, 2 * kTile);
@@ -472,13 +481,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma(tmem + T_DK, sdesc(dsa + off, kTile / 2, 1024), sdesc(qa + off, kTile / 2, 1024), id_mm,
                         (n > 0 || kk > 0));
                 }
+                commit(&qdo_empty);  // Q_n, dO_n consumed: the TMA refills them while dQ runs
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
                     const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
                 }
-                commit(&qdo_empty);  // Q_n, dO_n (and P, dS) consumed
-                commit(&dq_full);
+                commit(&dq_full);  // also: P, dS consumed
             }
         }
     } else {  // ---- softmax-gradient / dQ / dK dV epilogue (warps 2..5)
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = quad * 32 + lane;  // row: query within tile i (loop) / key within tile j (epilogue)
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
         for (int n = 0; n < n_iter; ++n) {
-            const int h = kvh * G + n / per_head, i = j + n % per_head;
+            const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
             const int qi = i * BQ + r;  // query index within the sequence
             const bool q_ok = qi < it.seq_len;
             const long long tok = static_cast<long long>(it.seq_start) + qi;
@@ -555,27 +564,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kj = j * BKV + r;
         const bool k_ok = kj < it.seq_len;
         const long long ktok = static_cast<long long>(it.seq_start) + kj;
-        for (int which = 0; which < 2; ++which) {
-            __nv_bfloat16* dst = (which ? g.dk : g.dv) + (ktok * g.KV + kvh) * HD;
+        for (int which = 0; which < 2; ++which) {  // partial dK / dV -> fp32 accumulators
+            float* dst = (which ? g.dk_acc : g.dv_acc) + (ktok * g.KV + kvh) * HD;
             const unsigned col = which ? T_DK : T_DV;
 #pragma unroll 1
-            for (int c = 0; c < HD; c += 32) {
-                unsigned v[32];
+            for (int c = 0; c < HD; c += 64) {
+                unsigned v[64];
                 TM_LD32(tmem + lane_base + col + c, v);
+                TM_LD32(tmem + lane_base + col + c + 32, (v + 32));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (k_ok) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint4 o;
-                        unsigned* w = reinterpret_cast<unsigned*>(&o);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(v[8 * q + 2 * e]),
-                                                                      __uint_as_float(v[8 * q + 2 * e + 1]));
-                            w[e] = *reinterpret_cast<unsigned*>(&hh);
-                        }
-                        *reinterpret_cast<uint4*>(dst + c + 8 * q) = o;
-                    }
+                    for (int e = 0; e < 64; e += 4)
+                        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c + e),
+                                     "f"(__uint_as_float(v[e])), "f"(__uint_as_float(v[e + 1])),
+                                     "f"(__uint_as_float(v[e + 2])), "f"(__uint_as_float(v[e + 3]))
+                                     : "memory");
                 }
             }
         }
@@ -704,10 +708,14 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
-        // workspace: D [H][T] fp32, then dq_acc [T][H][HD] fp32
+        // workspace (fp32): D [H][T] | dq_acc [T][H][HD] | dk_acc, dv_acc [T][KV][HD]
         float* D = static_cast<float*>(workspace);
-        float* dq_acc = D + (static_cast<long long>(H) * T + 63) / 64 * 64;  // keep the accumulator 256B-aligned
+        float* dq_acc = D + (static_cast<long long>(H) * T + 63) / 64 * 64;  // keep the accumulators 256B-aligned
+        float* dk_acc = dq_acc + T * H * HD;
+        float* dv_acc = dk_acc + T * KV * HD;
         const long long rows = T * H;
+        cudaError_t z = cudaMemsetAsync(dk_acc, 0, static_cast<size_t>(2 * T * KV * HD) * 4, st);
+        if (z != cudaSuccess) throw std::runtime_error(std::string("attn_bwd zero: ") + cudaGetErrorString(z));
         odc::count_launch();
         attn_bwd_prep_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
             static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), D, dq_acc, T, H);
@@ -718,7 +726,7 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             CUtensorMap mv = rows_map(v, static_cast<long long>(KV) * HD, T);
             CUtensorMap mdo = rows_map(dout, static_cast<long long>(H) * HD, T);
             BwdArgs a{};
-            a.items = static_cast<const Item*>(items);
+            a.items = static_cast<const BwdItem*>(items);
             a.H = H;
             a.KV = KV;
             a.scale = scale;
@@ -726,16 +734,21 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             a.lse = lse;
             a.D = D;
             a.dq_acc = dq_acc;
-            a.dk = static_cast<__nv_bfloat16*>(dk);
-            a.dv = static_cast<__nv_bfloat16*>(dv);
+            a.dk_acc = dk_acc;
+            a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
             attn_bwd_kernel<<<n_items, kThreads, kSmem, st>>>(mq, mk, mv, mdo, a);
         }
-        odc::count_launch();
-        const long long n4 = rows * HD / 4;
-        dq_convert_kernel<<<static_cast<unsigned>(std::min<long long>((n4 + 255) / 256, 148 * 8)), 256, 0, st>>>(
-            reinterpret_cast<const float4*>(dq_acc), static_cast<uint2*>(dq), n4);
+        auto convert = [&](const float* acc, void* out, long long n) {
+            odc::count_launch();
+            const long long n4 = n / 4;
+            dq_convert_kernel<<<static_cast<unsigned>(std::min<long long>((n4 + 255) / 256, 148 * 8)), 256, 0, st>>>(
+                reinterpret_cast<const float4*>(acc), static_cast<uint2*>(out), n4);
+        };
+        convert(dq_acc, dq, rows * HD);
+        convert(dk_acc, dk, T * KV * HD);
+        convert(dv_acc, dv, T * KV * HD);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw std::runtime_error(std::string("attn_bwd launch: ") + cudaGetErrorString(e));
     });

@@ -105,18 +105,29 @@ def attn_fwd(q, k, v, items, scale):
     return out, lse
 
 
-def attn_bwd_items(lens, KV: int, device) -> torch.Tensor:
-    """Backward work list: one item per (sequence, 128-key tile, kv head),
-    most query tiles (causal) first."""
-    items, start = [], 0
+def attn_bwd_items(lens, H: int, KV: int, device, sms: int = 148) -> torch.Tensor:
+    """Backward work list: per (sequence, 128-key tile, kv head) the causal loop
+    over (query head of the GQA group, query tile >= key tile). Loops longer
+    than ~1/(2*SMs) of the total are cut into chunks (their dK/dV partials meet
+    in fp32 accumulators) so the grid load-balances; largest first (LPT)."""
+    G = H // KV
+    loops, start = [], 0
     for n in lens:
         nt = (n + 127) // 128
         for kt in range(nt):
-            for h in range(KV):
-                items.append((start, n, kt, h, nt - kt))
+            loops.append((start, n, kt, G * (nt - kt)))
         start += n
-    items.sort(key=lambda t: -t[4])
-    return torch.tensor([t[:4] for t in items], dtype=torch.int32).to(device, non_blocking=True)
+    total = sum(t for *_, t in loops) * KV
+    chunk = max(32, -(-total // (2 * sms)))
+    items = []
+    for st, n, kt, t in loops:
+        pieces = -(-t // chunk)
+        for pc in range(pieces):
+            b, e = t * pc // pieces, t * (pc + 1) // pieces
+            for h in range(KV):
+                items.append((st, n, kt, h, b, e, 0, 0))
+    items.sort(key=lambda x: x[4] - x[5])
+    return torch.tensor(items, dtype=torch.int32).to(device, non_blocking=True)
 
 
 def attn_bwd(q, k, v, o, dout, lse, items, scale):
@@ -125,7 +136,7 @@ def attn_bwd(q, k, v, o, dout, lse, items, scale):
     dq = torch.empty_like(q)
     dk = torch.empty_like(k)
     dv = torch.empty_like(v)
-    ws = torch.empty((H * T + 63) // 64 * 64 + T * H * hd, dtype=torch.float32, device=q.device)
+    ws = torch.empty((H * T + 63) // 64 * 64 + T * H * hd + 2 * T * KV * hd, dtype=torch.float32, device=q.device)
     check(lib().odc_attn_bwd(_p(q), _p(k), _p(v), _p(o), _p(dout), _p(lse), _p(dq), _p(dk), _p(dv), _p(ws),
                              _p(items), items.shape[0], T, H, KV, hd, float(scale), _s()))
     return dq, dk, dv

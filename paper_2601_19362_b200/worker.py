@@ -266,7 +266,7 @@ def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, devic
 def attach_attn_items(b: Batch, seq_lens: Sequence[int], heads: int, device, kv_heads: int = 0) -> Batch:
     b.attn_items = F.attn_items(list(seq_lens), heads, device)
     if kv_heads:
-        b.attn_bwd_items = F.attn_bwd_items(list(seq_lens), kv_heads, device)
+        b.attn_bwd_items = F.attn_bwd_items(list(seq_lens), heads, kv_heads, device)
     return b
 
 

@@ -69,7 +69,7 @@ def test_attn_bwd_matches_reference(lens, H, KV):
     do = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
     scale = 128 ** -0.5
     out, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, DEV), scale)
-    dq, dk, dv = F.attn_bwd(q, k, v, out, do, lse, F.attn_bwd_items(lens, KV, DEV), scale)
+    dq, dk, dv = F.attn_bwd(q, k, v, out, do, lse, F.attn_bwd_items(lens, H, KV, DEV), scale)
     qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
     ro, _ = _ref(qf, kf, vf, lens, scale)
     ro.backward(do.float())

@@ -19,7 +19,7 @@ for lens in ([32768], [8192, 6000, 4000, 3000, 2000, 1024, 512, 512], [2048] * 1
     cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device="cuda")
     sc = 128 ** -0.5
     o, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, "cuda"), sc)
-    bi = F.attn_bwd_items(lens, KV, "cuda")
+    bi = F.attn_bwd_items(lens, H, KV, "cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     res = {"lens": lens[:3], "T": T}
     fl = sum(2 * 2 * s * s / 2 * 128 * H for s in lens) * 2.5

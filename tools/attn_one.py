@@ -16,6 +16,6 @@ do = torch.randn(T, H, 128, device="cuda").to(torch.bfloat16)
 sc = 128 ** -0.5
 for _ in range(2):
     o, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, "cuda"), sc)
-    F.attn_bwd(q, k, v, o, do, lse, F.attn_bwd_items(lens, KV, "cuda"), sc)
+    F.attn_bwd(q, k, v, o, do, lse, F.attn_bwd_items(lens, H, KV, "cuda"), sc)
 torch.cuda.synchronize()
 print("ok")
