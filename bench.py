@@ -380,7 +380,8 @@ def run_sft(args):
         roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": tflops_peak, "unit": "TFLOP/s",
                 "peak_kind": tkind, "frac": round(ach / tflops_peak, 4), "kernel": "odc::gemm::gemm_kernel (tcgen05)",
                 "launches": gm["launches"], "ms_per_launch": round(gm["ms"] / gm["launches"], 4),
-                "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": None}
+                "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": ncu_traffic("gemm::gemm_kernel<256>"),
+                "traffic_source": "profiles/r01/ncu_traffic.json (dram read+write per launch, ncu --set full)"}
     pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
     h2d = sum(16 * lens[i] + 8 + 16 * (shape.heads + shape.kv_heads) * ((lens[i] + 127) // 128)  # + attn work lists
               for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
@@ -415,6 +416,16 @@ def run_sft(args):
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/r01/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
+            return json.load(f)["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
 
 
 def comm_rates(eng, M, rank, world, dev, reps=10):
