@@ -119,3 +119,53 @@ def test_engine_multi_gpu(mode):
         p.join(timeout=60)
     bad = {r: m for r, m in res.items() if m != "ok"}
     assert not bad, "\n".join(f"rank {r}:\n{m}" for r, m in bad.items())
+
+
+def _timeout_worker(rank, world, port, q):
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from paper_2601_19362_b200 import errors as E
+        from paper_2601_19362_b200.engine import OdcEngine
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        eng = OdcEngine([4096], rank=rank, world=world, device=rank, timeout_s=2.0)
+        eng.set_params(0, torch.zeros(4096, device=dev))
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:  # rank 0 reaches the minibatch barrier; rank 1 never does
+            eng.minibatch_end()
+            try:
+                eng.check()
+                q.put((rank, "no timeout raised"))
+            except E.BarrierTimeout:
+                q.put((rank, "ok"))
+        else:
+            q.put((rank, "ok"))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.skipif(not have_gpus(2), reason="needs >= 2 GPUs")
+def test_barrier_watchdog_turns_a_missing_peer_into_an_error():
+    """SURVEY §5 failure detection: the device barrier spin is bounded by
+    %globaltimer; a peer that never arrives yields BarrierTimeout on the host
+    instead of a hung GPU."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
