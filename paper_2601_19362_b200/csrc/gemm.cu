@@ -363,6 +363,310 @@ CUtensorMap make_map(const void* base, long long inner, long long outer, long lo
     return m;
 }
 
+// ---------------------------------------------------------------- 2-CTA
+// cta_group::2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256
+// tile with M=256 UMMAs issued by the leader. Each CTA stages only its half of
+// A (128 rows) and its half of B (128 of the 256 N rows) per k-slice, so per-
+// SM smem traffic per MMA halves vs the 1-CTA 128 x 256 tile; each CTA's TMEM
+// holds its 128 accumulator rows x 256 columns (double-buffered).
+constexpr int kStages2 = 6;
+constexpr int kHalfBytes = 128 * BK * 2;          // 16 KB: 128 rows x 64 bf16
+constexpr int kStage2Bytes = 2 * kHalfBytes;      // A half + B half per CTA
+constexpr int kSmem2 = kStages2 * kStage2Bytes + 1024;
+
+__device__ __forceinline__ unsigned cta_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, unsigned long long* bar, void* smem, int c0,
+                                                int c1) {
+    // both CTAs load into their own smem; transaction bytes land on the leader's barrier
+    const unsigned mbar = su32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(su32(smem)),
+        "l"(map), "r"(c0), "r"(c1), "r"(mbar)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Args g) {
+    constexpr int BN2 = 256;
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) unsigned long long full_bar[kStages2], empty_bar[kStages2];
+    __shared__ __align__(8) unsigned long long tmem_full[2], tmem_empty[2];
+    __shared__ unsigned tmem_base;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const unsigned rank = cta_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x / 2, n_pairs = gridDim.x / 2;
+    const int num_items = g.tiles_m * g.tiles_n * g.splits;  // 256 x 256 tiles x K splits
+    const int k_tiles = static_cast<int>((g.K + BK - 1) / BK);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(&full_bar[s], 1);   // leader: one arrive.expect_tx for both CTAs' bytes
+            mbar_init(&empty_bar[s], 1);  // one multicast commit per use
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
+                     "n"(2 * BN2)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base;
+
+    auto coords = [&](int tile, int& m0, int& n0) {
+        constexpr int group = 8;
+        const int per_group = group * g.tiles_n;
+        const int gid = tile / per_group, first_m = gid * group;
+        const int gsize = min(group, g.tiles_m - first_m);
+        m0 = (first_m + (tile % per_group) % gsize) * 256;
+        n0 = ((tile % per_group) / gsize) * BN2;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (both CTAs: own A half, own B half)
+            int it = 0;
+            for (int w = pair; w < num_items; w += n_pairs) {
+                int m0, n0;
+                coords(w / g.splits, m0, n0);
+                const int sp = w % g.splits;
+                const int kb = k_tiles * sp / g.splits, ke = k_tiles * (sp + 1) / g.splits;
+                const int ma = m0 + static_cast<int>(rank) * 128, nb = n0 + static_cast<int>(rank) * 128;
+                for (int kt = kb; kt < ke; ++kt, ++it) {
+                    const int s = it % kStages2;
+                    if (it >= kStages2) mbar_wait(&empty_bar[s], ((it / kStages2) - 1) & 1);
+                    char* sa = smem + s * kStage2Bytes;
+                    char* sb = sa + kHalfBytes;
+                    if (leader) mbar_expect_tx(&full_bar[s], 2 * kStage2Bytes);
+                    const int k0 = kt * BK;
+                    if (!g.a_mn) {
+                        tma_load_2d_2sm(&map_a, &full_bar[s], sa, k0, ma);
+                    } else {
+                        tma_load_2d_2sm(&map_a, &full_bar[s], sa, ma, k0);
+                        tma_load_2d_2sm(&map_a, &full_bar[s], sa + 64 * BK * 2, ma + 64, k0);
+                    }
+                    if (!g.b_mn) {
+                        tma_load_2d_2sm(&map_b, &full_bar[s], sb, k0, nb);
+                    } else {
+                        tma_load_2d_2sm(&map_b, &full_bar[s], sb, nb, k0);
+                        tma_load_2d_2sm(&map_b, &full_bar[s], sb + 64 * BK * 2, nb + 64, k0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {  // ---- MMA issuer (leader only; M = 256 over both CTAs)
+            const unsigned idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(g.a_mn) << 15) |
+                                   (static_cast<unsigned>(g.b_mn) << 16) | (static_cast<unsigned>(BN2 >> 3) << 17) |
+                                   (static_cast<unsigned>(256 >> 4) << 24);
+            const unsigned a_lbo = g.a_mn ? BK * 128 : 16, b_lbo = g.b_mn ? BK * 128 : 16;
+            const unsigned a_step = g.a_mn ? 2048 : 32, b_step = g.b_mn ? 2048 : 32;
+            int it = 0, j = 0;
+            for (int w = pair; w < num_items; w += n_pairs, ++j) {
+                const int sp = w % g.splits;
+                const int kb = k_tiles * sp / g.splits, ke = k_tiles * (sp + 1) / g.splits;
+                const int acc = j & 1, use = j >> 1;
+                if (use > 0) mbar_wait(&tmem_empty[acc], (use - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned d_tmem = tmem + static_cast<unsigned>(acc * BN2);
+                for (int kt = kb; kt < ke; ++kt, ++it) {
+                    const int s = it % kStages2;
+                    mbar_wait(&full_bar[s], (it / kStages2) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned sa = su32(smem + s * kStage2Bytes);
+                    const unsigned sb = sa + kHalfBytes;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const std::uint64_t da = smem_desc(sa + kk * a_step, a_lbo, 1024);
+                        const std::uint64_t db = smem_desc(sb + kk * b_step, b_lbo, 1024);
+                        const unsigned accum = (kt > kb || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+                            "l"(da), "l"(db), "r"(idesc), "r"(accum)
+                            : "memory");
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                        "%1;" ::"r"(su32(&empty_bar[s])),
+                        "h"(static_cast<unsigned short>(3))
+                        : "memory");
+                }
+                asm volatile(
+                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                        su32(&tmem_full[acc])),
+                    "h"(static_cast<unsigned short>(3))
+                    : "memory");
+            }
+        }
+    } else {  // ---- epilogue warps 2..5: this CTA's 128 rows x 256 columns
+        const int quad = warp % 4;
+        unsigned leader_empty[2];
+        for (int a = 0; a < 2; ++a)
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty[a]) : "r"(su32(&tmem_empty[a])));
+        int j = 0;
+        for (int w = pair; w < num_items; w += n_pairs, ++j) {
+            const int acc = j & 1, use = j >> 1;
+            int m0, n0;
+            coords(w / g.splits, m0, n0);
+            mbar_wait(&tmem_full[acc], use & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const long long row = m0 + static_cast<long long>(rank) * 128 + quad * 32 + lane;
+            const bool row_ok = row < g.M;
+#pragma unroll 1
+            for (int c = 0; c < BN2; c += 32) {
+                unsigned r[32];
+                const unsigned taddr =
+                    tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2 + c);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c + 32 >= BN2) {  // accumulator in registers: release the buffer to the leader's MMA
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_empty[acc])
+                                     : "memory");
+                }
+                if (!row_ok) continue;
+                const long long col0 = n0 + c;
+                if (col0 >= g.N) continue;
+                const bool full = col0 + 32 <= g.N;
+                if (g.d_f32) {
+                    float* out = static_cast<float*>(g.D) + row * g.ldd + col0;
+                    if (g.splits > 1) {  // partial K range: reduce into D (zeroed or accumulated by the host)
+                        if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                            for (int q = 0; q < 32; q += 4)
+                                asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(out + q), "f"(__uint_as_float(r[q])),
+                                             "f"(__uint_as_float(r[q + 1])), "f"(__uint_as_float(r[q + 2])),
+                                             "f"(__uint_as_float(r[q + 3]))
+                                             : "memory");
+                        } else {
+                            for (int q = 0; q < 32 && col0 + q < g.N; ++q) atomicAdd(out + q, __uint_as_float(r[q]));
+                        }
+                    } else if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 4) {
+                            float4 v = make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]),
+                                                   __uint_as_float(r[q + 2]), __uint_as_float(r[q + 3]));
+                            if (g.accumulate) {
+                                const float4 o = *reinterpret_cast<const float4*>(out + q);
+                                v.x += o.x;
+                                v.y += o.y;
+                                v.z += o.z;
+                                v.w += o.w;
+                            }
+                            *reinterpret_cast<float4*>(out + q) = v;
+                        }
+                    } else {
+                        for (int q = 0; q < 32 && col0 + q < g.N; ++q)
+                            out[q] = __uint_as_float(r[q]) + (g.accumulate ? out[q] : 0.f);
+                    }
+                } else {
+                    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + col0;
+                    const __nv_bfloat16* add = g.C ? static_cast<const __nv_bfloat16*>(g.C) + row * g.ldd + col0
+                                                   : (g.accumulate ? out : nullptr);
+                    if (full && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 8) {
+                            uint4 v, a4 = make_uint4(0, 0, 0, 0);
+                            if (add) a4 = *reinterpret_cast<const uint4*>(add + q);
+                            const unsigned* aw = reinterpret_cast<const unsigned*>(&a4);
+                            unsigned* w = reinterpret_cast<unsigned*>(&v);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float lo = __uint_as_float(r[q + 2 * e]) + __uint_as_float(aw[e] << 16);
+                                const float hi = __uint_as_float(r[q + 2 * e + 1]) + __uint_as_float(aw[e] & 0xffff0000u);
+                                __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+                                w[e] = *reinterpret_cast<unsigned*>(&h);
+                            }
+                            *reinterpret_cast<uint4*>(out + q) = v;
+                        }
+                    } else {
+                        for (int q = 0; q < 32 && col0 + q < g.N; ++q) {
+                            float x = __uint_as_float(r[q]) + (add ? __bfloat162float(add[q]) : 0.f);
+                            out[q] = __float2bfloat16_rn(x);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync();  // the peer is done with our barriers / TMEM before dealloc
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN2) : "memory");
+    }
+}
+
+cudaError_t launch2(const void* A, const void* B, Args g, long long lda, long long ldb, cudaStream_t s) {
+    static thread_local int configured = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured != dev) {
+        cudaError_t e = cudaFuncSetAttribute(gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+        if (e != cudaSuccess) return e;
+        configured = dev;
+    }
+    // per CTA: A half = 128 rows (box 64 x 128 K-major / 2 boxes 64 x 64 MN-major), B half = 128 rows likewise
+    CUtensorMap ma = g.a_mn ? make_map(A, g.M, g.K, lda, 64, BK) : make_map(A, g.K, g.M, lda, BK, 128);
+    CUtensorMap mb = g.b_mn ? make_map(B, g.N, g.K, ldb, 64, BK) : make_map(B, g.K, g.N, ldb, BK, 128);
+    static int sms = 0;
+    if (!sms) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (const char* r = std::getenv("ODC_GEMM_RESERVE_SMS")) sms -= std::atoi(r);
+        sms &= ~1;
+        if (sms < 2) sms = 2;
+    }
+    g.tiles_m = static_cast<int>((g.M + 255) / 256);
+    g.tiles_n = static_cast<int>((g.N + 255) / 256);
+    const int pairs = g.tiles_m * g.tiles_n * g.splits;
+    const int grid = 2 * (pairs < sms / 2 ? pairs : sms / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem2;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, gemm2_kernel, ma, mb, g);
+}
+
 template <int BN>
 cudaError_t launch(const void* A, const void* B, const Args& g, long long lda, long long ldb, cudaStream_t s) {
     using C = Cfg<BN>;
@@ -418,16 +722,27 @@ extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const
         g.tiles_m = static_cast<int>((M + odc::gemm::BM - 1) / odc::gemm::BM);
         // split-K for fp32 outputs whose tile count cannot fill the GPU (wgrad of
         // d x d weights): partial tiles are reduced with red.global.add.v4.f32
+        static const bool two_cta = !std::getenv("ODC_GEMM_1CTA");
+        const bool use2 = two_cta && M >= 256 && N > 128;
+        // split-K for fp32 outputs whose tile count cannot fill the GPU (wgrad of
+        // d x d weights): partial tiles are reduced with red.global.add.v4.f32.
+        // The factor maximises the fraction of (pair-)slots busy in the last wave.
         g.splits = 1;
         {
-            const long long bn = N <= 128 ? 128 : 256;
-            const long long tiles = g.tiles_m * ((N + bn - 1) / bn);
+            const long long bm = use2 ? 256 : odc::gemm::BM, bn = (N <= 128 && !use2) ? 128 : 256;
+            const long long tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
             const long long kt = (K + odc::gemm::BK - 1) / odc::gemm::BK;
-            if (g.d_f32 && tiles < 120 && kt >= 8) {
-                long long sp = (148 + tiles - 1) / tiles;
-                sp = sp > 4 ? 4 : sp;
-                sp = sp > kt / 4 ? kt / 4 : sp;
-                g.splits = static_cast<int>(sp < 1 ? 1 : sp);
+            const long long slots = use2 ? 74 : 148;
+            if (g.d_f32 && tiles * 10 < slots * 8 && kt >= 8) {
+                double best = -1.0;
+                for (long long sp = 1; sp <= 4 && sp <= kt / 4; ++sp) {
+                    const long long items = tiles * sp, waves = (items + slots - 1) / slots;
+                    const double eff = static_cast<double>(items) / static_cast<double>(waves * slots);
+                    if (eff > best + 1e-9) {
+                        best = eff;
+                        g.splits = static_cast<int>(sp);
+                    }
+                }
             }
         }
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -437,7 +752,9 @@ extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const
             if (z != cudaSuccess) throw std::runtime_error(std::string("gemm split-K zero: ") + cudaGetErrorString(z));
         }
         cudaError_t e;
-        if (N <= 128) {
+        if (use2) {
+            e = odc::gemm::launch2(A, B, g, lda, ldb, st);
+        } else if (N <= 128) {
             g.tiles_n = static_cast<int>((N + 127) / 128);
             e = odc::gemm::launch<128>(A, B, g, lda, ldb, st);
         } else {
