@@ -393,6 +393,28 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, unsigned
         : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, unsigned* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+// Pins the registers of an asynchronous tcgen05.ld after its wait::ld: every use depends on this asm.
+__device__ __forceinline__ void reg_fence32(unsigned* r) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Args g) {
     constexpr int BN2 = 256;
@@ -528,10 +550,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = j & 1, use = j >> 1;
             int m0, n0;
             coords(w / g.splits, m0, n0);
-            mbar_wait(&tmem_full[acc], use & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const long long row = m0 + static_cast<long long>(rank) * 128 + quad * 32 + lane;
             const bool row_ok = row < g.M;
+            // fast path (bf16 output, whole 256-column row in range, 16-B aligned): the residual row is
+            // prefetched into registers while the MMAs run, TMEM loads are double-buffered.
+            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + n0;
+            const __nv_bfloat16* arow = g.C ? static_cast<const __nv_bfloat16*>(g.C) + row * g.ldd + n0
+                                            : (g.accumulate ? orow : nullptr);
+            const bool fast = !g.d_f32 && n0 + BN2 <= g.N && (reinterpret_cast<uintptr_t>(orow) & 15) == 0 &&
+                              (arow == nullptr || (reinterpret_cast<uintptr_t>(arow) & 15) == 0);
+            if (fast) {
+                uint4 cb[BN2 / 8];
+                if (arow && row_ok) {
+#pragma unroll
+                    for (int i = 0; i < BN2 / 8; ++i) cb[i] = __ldg(reinterpret_cast<const uint4*>(arow) + i);
+                }
+                mbar_wait(&tmem_full[acc], use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned tbase = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2);
+                unsigned ra[32], rb[32];
+                tmem_ld32(tbase, ra);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                reg_fence32(ra);
+#pragma unroll
+                for (int c = 0; c < BN2 / 32; ++c) {
+                    unsigned* cur = (c & 1) ? rb : ra;
+                    unsigned* nxt = (c & 1) ? ra : rb;
+                    if (c + 1 < BN2 / 32) tmem_ld32(tbase + (c + 1) * 32, nxt);
+                    if (c + 1 == BN2 / 32) {  // last chunk in registers: release the buffer to the leader's MMA
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                             leader_empty[acc])
+                                         : "memory");
+                    }
+                    if (row_ok) {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 8) {
+                            uint4 v;
+                            const uint4 a4 = arow ? cb[c * 4 + q / 8] : make_uint4(0, 0, 0, 0);
+                            const unsigned* aw = reinterpret_cast<const unsigned*>(&a4);
+                            unsigned* w = reinterpret_cast<unsigned*>(&v);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float lo = __uint_as_float(cur[q + 2 * e]) + __uint_as_float(aw[e] << 16);
+                                const float hi = __uint_as_float(cur[q + 2 * e + 1]) + __uint_as_float(aw[e] & 0xffff0000u);
+                                __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+                                w[e] = *reinterpret_cast<unsigned*>(&h);
+                            }
+                            *reinterpret_cast<uint4*>(orow + c * 32 + q) = v;
+                        }
+                    }
+                    if (c + 1 < BN2 / 32) {
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        reg_fence32(nxt);
+                    }
+                }
+                continue;
+            }
+            mbar_wait(&tmem_full[acc], use & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
             for (int c = 0; c < BN2; c += 32) {
                 unsigned r[32];

@@ -21,7 +21,7 @@ def _p(t):
 
 class Recorder:
     """Optional live timing of every GEMM launch (CUDA events on the launching
-    stream) for the bench's roofline: records (flops, start, end)."""
+    stream) for the bench's roofline: records (flops, start, end, shape key)."""
 
     def __init__(self):
         self.rows = []
@@ -29,8 +29,8 @@ class Recorder:
     def summary(self):
         if not self.rows:
             return None
-        ms = [s.elapsed_time(e) for _, s, e in self.rows]
-        fl = sum(f for f, _, _ in self.rows)
+        ms = [r[1].elapsed_time(r[2]) for r in self.rows]
+        fl = sum(r[0] for r in self.rows)
         return {"launches": len(self.rows), "flops": fl, "ms": sum(ms)}
 
 
@@ -51,7 +51,8 @@ def gemm(a, b, out, M, N, K, lda, ldb, a_mn, b_mn, accumulate=False, stream=None
     if rec is not None:
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(s)
-        rec.rows.append((2.0 * M * N * K, e0, e1))
+        rec.rows.append((2.0 * M * N * K, e0, e1, (M, N, K, int(a_mn), int(b_mn), out.dtype == torch.float32,
+                                                    bool(accumulate), residual is not None)))
     return out
 
 

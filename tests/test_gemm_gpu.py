@@ -37,3 +37,22 @@ def test_accumulate_f32(T, inn, out):
     want = acc + dy.float().t() @ x.float()
     G.linear_wgrad(dy, x, out=acc, accumulate=True)
     torch.testing.assert_close(acc, want, rtol=2e-3, atol=2e-3 * (T / 64) ** 0.5)
+
+
+@pytest.mark.parametrize("T,inn,out", [(1000, 1536, 1536), (333, 256, 320), (4096, 512, 2048)])
+def test_fwd_residual_epilogue(T, inn, out):
+    """y = x·wᵀ + r fused in the epilogue (residual row prefetched into
+    registers on the 2-CTA fast path; generic path on the ragged N tail)."""
+    x, w, r = _r(T, inn), _r(out, inn), _r(T, out)
+    y = G.linear_fwd(x, w, residual=r)
+    want = x.float() @ w.float().t() + r.float()
+    torch.testing.assert_close(y.float(), want, rtol=1e-2, atol=2e-2 * (inn / 64) ** 0.5)
+
+
+def test_bf16_accumulate_in_place():
+    T, inn, out = 1024, 384, 768
+    x, w = _r(T, inn), _r(out, inn)
+    y = _r(T, out)
+    want = x.float() @ w.float().t() + y.float()
+    G.gemm(x, w, y, T, out, inn, x.stride(0), w.stride(0), False, False, accumulate=True)
+    torch.testing.assert_close(y.float(), want, rtol=1e-2, atol=2e-2 * (inn / 64) ** 0.5)
