@@ -382,9 +382,34 @@ __device__ __forceinline__ void store_swizzled(char* tile, int r, int c, const u
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 elementwise (2 per TMEM lane quadrant)
+
+__device__ __forceinline__ void bar_ew() {  // named barrier over the 8 elementwise warps
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ void tma_reduce_add(const CUtensorMap* map, const void* smem, int c0, int c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+                 "r"(c0), "r"(c1), "r"(su32(smem))
+                 : "memory");
+}
+// 64 fp32 columns [c0, c0+64) of row r into an fp32 staging tile made of four [128 rows][32 fp32] 128B-swizzled
+// chunks (the box layout of an f32 tensor map with SWIZZLE_128B): conflict-free 16-B stores.
+__device__ __forceinline__ void stage_f32(char* stage, int r, int c0, const unsigned* v) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        char* row = stage + ((c0 >> 5) + k) * (kTile / 2) + r * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(row + ((q ^ (r & 7)) << 4)) =
+                make_uint4(v[32 * k + 4 * q], v[32 * k + 4 * q + 1], v[32 * k + 4 * q + 2], v[32 * k + 4 * q + 3]);
+    }
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do, BwdArgs g) {
+                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                    const __grid_constant__ CUtensorMap map_dq, const __grid_constant__ CUtensorMap map_dk,
+                    const __grid_constant__ CUtensorMap map_dv, BwdArgs g) {
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     char* sK = smem;
@@ -393,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     char* sdO = smem + 3 * kTile;
     char* sP = smem + 4 * kTile;
     char* sdS = smem + 5 * kTile;
+    char* stage = sP;  // [sP, sdS] = 64 KB fp32 staging of dQ_n once every MMA of n is done
     // sdp_full: S_n and dP_n in TMEM; ds_full: P_n / dS_n in smem (S_n, dP_n consumed);
     // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
     __shared__ __align__(8) unsigned long long kv_full, qdo_full, qdo_empty, sdp_full, ds_full, dq_full, dq_read;
@@ -413,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&qdo_full, 1);
         mbar_init(&qdo_empty, 1);
         mbar_init(&sdp_full, 1);
-        mbar_init(&ds_full, 4);
+        mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
-        mbar_init(&dq_read, 4);
+        mbar_init(&dq_read, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -456,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            dsa = su32(sdS);
             for (int n = 0; n < n_iter; ++n) {
                 mbar_wait(&qdo_full, n & 1);
-                // S columns were consumed by softmax(n-1) before its ds_full (waited below at n-1)
+                // S columns were consumed by the elementwise warps (n-1) before their ds_full (waited below at n-1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {  // S = Q K^T (overlaps the dQ_{n-1} read-out)
@@ -490,98 +516,103 @@ __global__ void __launch_bounds__(kThreads, 1)
                 commit(&dq_full);  // also: P, dS consumed
             }
         }
-    } else {  // ---- softmax-gradient / dQ / dK dV epilogue (warps 2..5)
+    } else {  // ---- elementwise / dQ / dK dV epilogue (warps 2..9): row quadrant warp%4, column half (warp-2)/4
         const int quad = warp % 4;
+        const int c0 = ((warp - 2) >> 2) * 64;  // this warp's 64 columns
+        const bool lead = warp == 2 && lane == 0;  // issues the TMA reductions
         const int r = quad * 32 + lane;  // row: query within tile i (loop) / key within tile j (epilogue)
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
+        const float sl2 = g.scale_log2, sc = g.scale;
         for (int n = 0; n < n_iter; ++n) {
             const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
             const int qi = i * BQ + r;  // query index within the sequence
             const bool q_ok = qi < it.seq_len;
             const long long tok = static_cast<long long>(it.seq_start) + qi;
             const float lse2 = q_ok ? g.lse[static_cast<long long>(h) * g.T + tok] * kLog2e : 0.f;
-            const float Dr = q_ok ? g.D[static_cast<long long>(h) * g.T + tok] : 0.f;
-            const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV : -1;  // visible keys of tile j
+            const float Ds = q_ok ? g.D[static_cast<long long>(h) * g.T + tok] * sc : 0.f;
+            const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV - c0 : -1;  // visible keys among our columns
             mbar_wait(&sdp_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-            for (int c = 0; c < BKV; c += 64) {  // 64-column halves: 4 TMEM loads, one wait
-                unsigned sv[64], dp[64];
-                TM_LD32(tmem + lane_base + T_S + c, sv);
-                TM_LD32(tmem + lane_base + T_S + c + 32, (sv + 32));
-                TM_LD32(tmem + lane_base + T_DP + c, dp);
-                TM_LD32(tmem + lane_base + T_DP + c + 32, (dp + 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            unsigned sv[64], dp[64];
+            TM_LD32(tmem + lane_base + T_S + c0, sv);
+            TM_LD32(tmem + lane_base + T_S + c0 + 32, (sv + 32));
+            TM_LD32(tmem + lane_base + T_DP + c0, dp);
+            TM_LD32(tmem + lane_base + T_DP + c0 + 32, (dp + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // P = exp2(S*scale*log2e - lse2) (0 where masked), dS = P * (dP*scale - D*scale), packed bf16 in place
 #pragma unroll
-                for (int half = 0; half < 64; half += 32) {
-                    unsigned pk[16], dk2[16];
-#pragma unroll
-                    for (int e = 0; e < 32; e += 2) {
-                        const int x = half + e;
-                        float p0 = ex2(__uint_as_float(sv[x]) * g.scale_log2 - lse2);
-                        float p1 = ex2(__uint_as_float(sv[x + 1]) * g.scale_log2 - lse2);
-                        if (c + x > lim) p0 = 0.f;
-                        if (c + x + 1 > lim) p1 = 0.f;
-                        const float d0 = g.scale * p0 * (__uint_as_float(dp[x]) - Dr);
-                        const float d1 = g.scale * p1 * (__uint_as_float(dp[x + 1]) - Dr);
-                        __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
-                        pk[e / 2] = *reinterpret_cast<unsigned*>(&hp);
-                        dk2[e / 2] = *reinterpret_cast<unsigned*>(&hd);
-                    }
-                    store_swizzled(sP, r, c + half, pk);
-                    store_swizzled(sdS, r, c + half, dk2);
-                }
+            for (int x = 0; x < 64; x += 2) {
+                float p0 = ex2(fmaf(__uint_as_float(sv[x]), sl2, -lse2));
+                float p1 = ex2(fmaf(__uint_as_float(sv[x + 1]), sl2, -lse2));
+                if (x > lim) p0 = 0.f;
+                if (x + 1 > lim) p1 = 0.f;
+                const float d0 = p0 * fmaf(__uint_as_float(dp[x]), sc, -Ds);
+                const float d1 = p1 * fmaf(__uint_as_float(dp[x + 1]), sc, -Ds);
+                __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
+                sv[x / 2] = *reinterpret_cast<unsigned*>(&hp);
+                dp[x / 2] = *reinterpret_cast<unsigned*>(&hd);
             }
+            if (n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
+                if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                bar_ew();
+            }
+            store_swizzled(sP, r, c0, sv);
+            store_swizzled(sP, r, c0 + 32, sv + 16);
+            store_swizzled(sdS, r, c0, dp);
+            store_swizzled(sdS, r, c0 + 32, dp + 16);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&ds_full);
-            // dQ_n (fp32, already scaled) -> global accumulator, while the MMA warp starts S_{n+1}
+            // dQ_n (fp32, already scaled) -> smem staging -> TMA reduce-add into the global accumulator,
+            // while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float* dqrow = g.dq_acc + (tok * g.H + h) * HD;
-#pragma unroll 1
-            for (int c = 0; c < HD; c += 64) {
-                unsigned v[64];
-                TM_LD32(tmem + lane_base + T_DP + c, v);
-                TM_LD32(tmem + lane_base + T_DP + c + 32, (v + 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (q_ok) {
-#pragma unroll
-                    for (int e = 0; e < 64; e += 4)
-                        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c + e),
-                                     "f"(__uint_as_float(v[e])), "f"(__uint_as_float(v[e + 1])),
-                                     "f"(__uint_as_float(v[e + 2])), "f"(__uint_as_float(v[e + 3]))
-                                     : "memory");
-                }
-            }
+            unsigned v[64];
+            TM_LD32(tmem + lane_base + T_DP + c0, v);
+            TM_LD32(tmem + lane_base + T_DP + c0 + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&dq_read);
-        }
-        // dK, dV of the key tile (complete: the last dq_full covers every MMA)
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int kj = j * BKV + r;
-        const bool k_ok = kj < it.seq_len;
-        const long long ktok = static_cast<long long>(it.seq_start) + kj;
-        for (int which = 0; which < 2; ++which) {  // partial dK / dV -> fp32 accumulators
-            float* dst = (which ? g.dk_acc : g.dv_acc) + (ktok * g.KV + kvh) * HD;
-            const unsigned col = which ? T_DK : T_DV;
-#pragma unroll 1
-            for (int c = 0; c < HD; c += 64) {
-                unsigned v[64];
-                TM_LD32(tmem + lane_base + col + c, v);
-                TM_LD32(tmem + lane_base + col + c + 32, (v + 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (k_ok) {
+            stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_ew();
+            if (lead) {
+                const int row0 = it.seq_start + i * BQ;
 #pragma unroll
-                    for (int e = 0; e < 64; e += 4)
-                        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c + e),
-                                     "f"(__uint_as_float(v[e])), "f"(__uint_as_float(v[e + 1])),
-                                     "f"(__uint_as_float(v[e + 2])), "f"(__uint_as_float(v[e + 3]))
-                                     : "memory");
-                }
+                for (int k = 0; k < 4; ++k) tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
+        }
+        // dK, dV of the key tile (complete: the last dq_full covers every MMA) -> staging -> TMA reduce-add
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        bar_ew();
+        char* st_dv = sP;  // [sP, sdS]
+        char* st_dk = sQ;  // [sQ, sdO]: Q / dO are no longer read
+        {
+            unsigned v[64];
+            TM_LD32(tmem + lane_base + T_DV + c0, v);
+            TM_LD32(tmem + lane_base + T_DV + c0 + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            stage_f32(st_dv, r, c0, v);
+            TM_LD32(tmem + lane_base + T_DK + c0, v);
+            TM_LD32(tmem + lane_base + T_DK + c0 + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            stage_f32(st_dk, r, c0, v);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_ew();
+        if (lead) {
+            const int krow0 = it.seq_start + j * BKV;  // key rows past the sequence end hold exact zeros
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                tma_reduce_add(&map_dv, st_dv + k * (kTile / 2), kvh * HD + 32 * k, krow0);
+                tma_reduce_add(&map_dk, st_dk + k * (kTile / 2), kvh * HD + 32 * k, krow0);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -650,6 +681,21 @@ CUtensorMap rows_map(const void* base, long long cols, long long rows) {
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw odcsim::ParamError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+// fp32 [rows][cols] accumulator as the target of TMA reduce-add: box {32 fp32 = 128 B, 128 rows}, 128B swizzle
+CUtensorMap f32_rows_map(void* base, long long cols, long long rows) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw odcsim::ParamError("cuTensorMapEncodeTiled (f32) failed (" + std::to_string(r) + ")");
     return m;
 }
 
@@ -725,6 +771,9 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             CUtensorMap mk = rows_map(k, static_cast<long long>(KV) * HD, T);
             CUtensorMap mv = rows_map(v, static_cast<long long>(KV) * HD, T);
             CUtensorMap mdo = rows_map(dout, static_cast<long long>(H) * HD, T);
+            CUtensorMap mdq = f32_rows_map(dq_acc, static_cast<long long>(H) * HD, T);
+            CUtensorMap mdk = f32_rows_map(dk_acc, static_cast<long long>(KV) * HD, T);
+            CUtensorMap mdv = f32_rows_map(dv_acc, static_cast<long long>(KV) * HD, T);
             BwdArgs a{};
             a.items = static_cast<const BwdItem*>(items);
             a.H = H;
@@ -738,7 +787,7 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
-            attn_bwd_kernel<<<n_items, kThreads, kSmem, st>>>(mq, mk, mv, mdo, a);
+            attn_bwd_kernel<<<n_items, kBwdThreads, kSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
         auto convert = [&](const float* acc, void* out, long long n) {
             odc::count_launch();
