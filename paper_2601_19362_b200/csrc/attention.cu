@@ -382,7 +382,8 @@ __device__ __forceinline__ void store_swizzled(char* tile, int r, int c, const u
     }
 }
 
-constexpr int kBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 elementwise (2 per TMEM lane quadrant)
+constexpr int kBwdThreads = 320;
+constexpr int kBwdSmem = kTile * 7 + 1024;  // K, V, Q x2, dO, P, dS  // warp 0 TMA, warp 1 MMA, warps 2-9 elementwise (2 per TMEM lane quadrant)
 
 __device__ __forceinline__ void bar_ew() {  // named barrier over the 8 elementwise warps
     asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -414,14 +415,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     char* sK = smem;
     char* sV = smem + kTile;
-    char* sQ = smem + 2 * kTile;
-    char* sdO = smem + 3 * kTile;
-    char* sP = smem + 4 * kTile;
-    char* sdS = smem + 5 * kTile;
+    char* sQ0 = smem + 2 * kTile;  // Q double-buffered (sQ0 + b * kTile): Q_{n+1} lands while n computes
+    char* sdO = smem + 4 * kTile;
+    char* sP = smem + 5 * kTile;
+    char* sdS = smem + 6 * kTile;
     char* stage = sP;  // [sP, sdS] = 64 KB fp32 staging of dQ_n once every MMA of n is done
     // sdp_full: S_n and dP_n in TMEM; ds_full: P_n / dS_n in smem (S_n, dP_n consumed);
     // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
-    __shared__ __align__(8) unsigned long long kv_full, qdo_full, qdo_empty, sdp_full, ds_full, dq_full, dq_read;
+    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, ds_full,
+        dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
     const BwdItem it = g.items[blockIdx.x];
@@ -436,8 +438,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
     if (warp == 0 && lane == 0) {
         mbar_init(&kv_full, 1);
-        mbar_init(&qdo_full, 1);
-        mbar_init(&qdo_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&q_full[b], 1);
+            mbar_init(&q_empty[b], 1);
+        }
+        mbar_init(&do_full, 1);
+        mbar_init(&do_empty, 1);
         mbar_init(&sdp_full, 1);
         mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
@@ -465,23 +471,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tma_2d(&map_v, &kv_full, sV + kTile / 2, kvh * HD + 64, k0);
             for (int n = 0; n < n_iter; ++n) {
                 const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
-                if (n > 0) mbar_wait(&qdo_empty, (n - 1) & 1);
-                const int q0 = it.seq_start + i * BQ;
-                mbar_expect_tx(&qdo_full, 2 * kTile);
-                tma_2d(&map_q, &qdo_full, sQ, h * HD, q0);
-                tma_2d(&map_q, &qdo_full, sQ + kTile / 2, h * HD + 64, q0);
-                tma_2d(&map_do, &qdo_full, sdO, h * HD, q0);
-                tma_2d(&map_do, &qdo_full, sdO + kTile / 2, h * HD + 64, q0);
+                const int q0 = it.seq_start + i * BQ, b = n & 1;
+                if (n >= 2) mbar_wait(&q_empty[b], ((n >> 1) - 1) & 1);  // Q_{n-2} consumed by dK_{n-2}
+                mbar_expect_tx(&q_full[b], kTile);
+                tma_2d(&map_q, &q_full[b], sQ0 + b * kTile, h * HD, q0);
+                tma_2d(&map_q, &q_full[b], sQ0 + b * kTile + kTile / 2, h * HD + 64, q0);
+                if (n >= 1) mbar_wait(&do_empty, (n - 1) & 1);  // dO_{n-1} consumed by dV_{n-1}
+                mbar_expect_tx(&do_full, kTile);
+                tma_2d(&map_do, &do_full, sdO, h * HD, q0);
+                tma_2d(&map_do, &do_full, sdO + kTile / 2, h * HD + 64, q0);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             const unsigned id_kk = instr(0, 0), id_mm = instr(1, 1), id_km = instr(0, 1);
             mbar_wait(&kv_full, 0);
-            const unsigned qa = su32(sQ), doa = su32(sdO), ka = su32(sK), va = su32(sV), pa = su32(sP),
-                           dsa = su32(sdS);
+            const unsigned doa = su32(sdO), ka = su32(sK), va = su32(sV), pa = su32(sP), dsa = su32(sdS);
             for (int n = 0; n < n_iter; ++n) {
-                mbar_wait(&qdo_full, n & 1);
+                const int b = n & 1;
+                const unsigned qa = su32(sQ0 + b * kTile);
+                mbar_wait(&q_full[b], (n >> 1) & 1);
                 // S columns were consumed by the elementwise warps (n-1) before their ds_full (waited below at n-1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
@@ -490,6 +499,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma(tmem + T_S, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_kk, kk > 0);
                 }
                 if (n > 0) mbar_wait(&dq_read, (n - 1) & 1);  // dP columns free again
+                mbar_wait(&do_full, n & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {  // dP = dO V^T
@@ -500,14 +510,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 mbar_wait(&ds_full, n & 1);  // P, dS in smem; S, dP read
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int kk = 0; kk < BQ / 16; ++kk) {  // K = query rows: MN-major A (P^T, dS^T) and B (dO, Q)
-                    const unsigned off = kk * 2048;
-                    mma(tmem + T_DV, sdesc(pa + off, kTile / 2, 1024), sdesc(doa + off, kTile / 2, 1024), id_mm,
-                        (n > 0 || kk > 0));
-                    mma(tmem + T_DK, sdesc(dsa + off, kTile / 2, 1024), sdesc(qa + off, kTile / 2, 1024), id_mm,
-                        (n > 0 || kk > 0));
-                }
-                commit(&qdo_empty);  // Q_n, dO_n consumed: the TMA refills them while dQ runs
+                for (int kk = 0; kk < BQ / 16; ++kk)  // K = query rows: MN-major A (P^T) and B (dO)
+                    mma(tmem + T_DV, sdesc(pa + kk * 2048, kTile / 2, 1024), sdesc(doa + kk * 2048, kTile / 2, 1024),
+                        id_mm, (n > 0 || kk > 0));
+                commit(&do_empty);  // dO_n consumed: the TMA refills it while dK, dQ run
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
+                    mma(tmem + T_DK, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024),
+                        id_mm, (n > 0 || kk > 0));
+                commit(&q_empty[b]);
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
                     const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         bar_ew();
         char* st_dv = sP;  // [sP, sdS]
-        char* st_dk = sQ;  // [sQ, sdO]: Q / dO are no longer read
+        char* st_dk = sQ0;  // both Q buffers: Q is no longer read
         {
             unsigned v[64];
             TM_LD32(tmem + lane_base + T_DV + c0, v);
@@ -750,7 +761,7 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
         int dev = 0;
         cudaGetDevice(&dev);
         if (configured != dev) {
-            cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
             if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
@@ -787,7 +798,7 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
-            attn_bwd_kernel<<<n_items, kBwdThreads, kSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
+            attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
         auto convert = [&](const float* acc, void* out, long long n) {
             odc::count_launch();

@@ -542,9 +542,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {  // ---- epilogue warps 2..5: this CTA's 128 rows x 256 columns
         const int quad = warp % 4;
-        unsigned leader_empty[2];
-        for (int a = 0; a < 2; ++a)
-            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty[a]) : "r"(su32(&tmem_empty[a])));
+        unsigned leader_empty0;  // the leader CTA's tmem_empty[0] (tmem_empty[1] is 8 bytes above)
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(su32(&tmem_empty[0])));
         int j = 0;
         for (int w = pair; w < num_items; w += n_pairs, ++j) {
             const int acc = j & 1, use = j >> 1;
@@ -582,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0)
                             asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                                             leader_empty[acc])
+                                             leader_empty0 + 8u * acc)
                                          : "memory");
                     }
                     if (row_ok) {
@@ -630,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
                     if (lane == 0)
-                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_empty[acc])
+                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_empty0 + 8u * acc)
                                      : "memory");
                 }
                 if (!row_ok) continue;
