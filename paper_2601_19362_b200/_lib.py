@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libodc.so")
+LIB_PATH = os.environ.get("ODC_LIB_PATH") or os.path.join(PKG, "lib", "libodc.so")  # override: A/B variant builds
 
 ODC_OK, ODC_ERR_PARAM, ODC_ERR_INFEASIBLE, ODC_ERR_INVARIANT = 0, 2, 3, 4
 ODC_ERR_PROTOCOL, ODC_ERR_STATE, ODC_ERR_MODE, ODC_ERR_CUDA, ODC_ERR_TIMEOUT = 5, 6, 7, 8, 9

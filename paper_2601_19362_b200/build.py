@@ -48,14 +48,18 @@ def _run(cmd, log):
         raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + p.stdout)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, variant: str | None = None, defines=()) -> str:
+    """variant: an A/B build with extra -D defines into lib/variants/<variant>/libodc.so
+    (selected at run time with ODC_LIB_PATH); the default build is lib/libodc.so."""
     cu, cpp, hdr = _sources()
-    if not force and not _stale(LIB, cu + cpp + hdr + [__file__]):
-        return LIB
-    objdir = os.path.join(LIBDIR, "obj")
+    libdir = LIBDIR if variant is None else os.path.join(LIBDIR, "variants", variant)
+    lib = os.path.join(libdir, "libodc.so")
+    if not force and not _stale(lib, cu + cpp + hdr + [__file__]):
+        return lib
+    objdir = os.path.join(libdir, "obj")
     os.makedirs(objdir, exist_ok=True)
     log, objs = [], []
-    inc = ["-I" + INCLUDE, "-I" + CSRC]
+    inc = ["-I" + INCLUDE, "-I" + CSRC] + ["-D" + d for d in defines]
     from concurrent.futures import ThreadPoolExecutor
 
     jobs = []
@@ -71,14 +75,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
             jobs.append([NVCC, *ARCH, *NVFLAGS, *inc, "-c", src, "-o", obj])
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(lambda c: _run(c, log), jobs))
-    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", LIB, *objs,
+    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", lib, *objs,
           "-Xlinker", "-rpath," + os.path.join(CUDA, "lib64"), "-lcuda"], log)
-    with open(os.path.join(LIBDIR, "build.log"), "w") as f:
+    with open(os.path.join(libdir, "build.log"), "w") as f:
         f.write("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    # python -m paper_2601_19362_b200.build [-v] [-f] [--variant NAME DEFINE ...]
+    args = sys.argv[1:]
+    var, defs = None, []
+    if "--variant" in args:
+        i = args.index("--variant")
+        var, defs = args[i + 1], [a for a in args[i + 2:] if not a.startswith("-")]
+    print(build(verbose="-v" in args, force="-f" in args, variant=var, defines=defs))

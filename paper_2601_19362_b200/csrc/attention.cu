@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -50,12 +51,37 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
     asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
+#ifdef ODC_ATTN_DEBUG
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    bool said = false;
+    while (true) {
+        unsigned ok;
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (!said && t - t0 > 2000000000ull) {
+            if (threadIdx.x % 32 == 0)
+                printf("attn hang: block %d thread %d bar smem 0x%x parity %u\n", blockIdx.x, threadIdx.x, su32(b), parity);
+            said = true;
+        }
+        if (t - t0 > 6000000000ull) asm volatile("trap;");
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
     asm volatile(
         "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(su32(b)),
         "r"(parity)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void tma_2d(const CUtensorMap* map, unsigned long long* bar, void* smem, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -91,6 +117,30 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// packed fp32x2 FMA / MUL (FFMA2 / FMUL2 on sm_100): two lanes of math per issue slot
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+        "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmul.rn.f32x2 rd, ra, rb;\n"
+        "mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ unsigned pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<unsigned*>(&h);
+}
+__device__ __forceinline__ void sts128(const void* p, unsigned a, unsigned b, unsigned c, unsigned d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(su32(p)), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 __device__ __forceinline__ void commit(unsigned long long* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
@@ -292,8 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int chunk = ((c & 63) >> 3) + q;
-                    *reinterpret_cast<uint4*>(half + ((chunk ^ (r & 7)) << 4)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    sts128(half + ((chunk ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
@@ -377,13 +426,14 @@ __device__ __forceinline__ void store_swizzled(char* tile, int r, int c, const u
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int chunk = ((c & 63) >> 3) + q;
-        *reinterpret_cast<uint4*>(half + ((chunk ^ (r & 7)) << 4)) =
-            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        sts128(half + ((chunk ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
     }
 }
 
-constexpr int kBwdThreads = 320;
-constexpr int kBwdSmem = kTile * 7 + 1024;  // K, V, Q x2, dO, P, dS  // warp 0 TMA, warp 1 MMA, warps 2-9 elementwise (2 per TMEM lane quadrant)
+// warp 0 TMA, warp 1 MMA (warpgroup 0, registers given away with setmaxnreg), warps 4-11 elementwise
+// (two warpgroups, one per 64-column half; each covers the four TMEM lane quadrants)
+constexpr int kBwdThreads = 384;
+constexpr int kBwdSmem = kTile * 7 + 1024;  // K, V, Q x2, dO, P, dS
 
 __device__ __forceinline__ void bar_ew() {  // named barrier over the 8 elementwise warps
     asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -401,8 +451,8 @@ __device__ __forceinline__ void stage_f32(char* stage, int r, int c0, const unsi
         char* row = stage + ((c0 >> 5) + k) * (kTile / 2) + r * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<uint4*>(row + ((q ^ (r & 7)) << 4)) =
-                make_uint4(v[32 * k + 4 * q], v[32 * k + 4 * q + 1], v[32 * k + 4 * q + 2], v[32 * k + 4 * q + 3]);
+            sts128(row + ((q ^ (r & 7)) << 4), v[32 * k + 4 * q], v[32 * k + 4 * q + 1], v[32 * k + 4 * q + 2],
+                   v[32 * k + 4 * q + 3]);
     }
 }
 
@@ -422,8 +472,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     char* stage = sP;  // [sP, sdS] = 64 KB fp32 staging of dQ_n once every MMA of n is done
     // sdp_full: S_n and dP_n in TMEM; ds_full: P_n / dS_n in smem (S_n, dP_n consumed);
     // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
-    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, ds_full,
-        dq_full, dq_read;
+    // s_read: S_n, dP_n are in the elementwise warps' registers (S columns free for S_{n+1})
+    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, s_read,
+        ds_full, dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
     const BwdItem it = g.items[blockIdx.x];
@@ -445,6 +496,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_init(&do_full, 1);
         mbar_init(&do_empty, 1);
         mbar_init(&sdp_full, 1);
+        mbar_init(&s_read, 8);
+#ifdef ODC_ATTN_DEBUG
+        if (blockIdx.x == 0)
+            printf("bars: kv_full %x q_full %x %x q_empty %x %x do_full %x do_empty %x sdp_full %x s_read %x ds_full %x "
+                   "dq_full %x dq_read %x n_iter %d\n",
+                   su32(&kv_full), su32(&q_full[0]), su32(&q_full[1]), su32(&q_empty[0]), su32(&q_empty[1]),
+                   su32(&do_full), su32(&do_empty), su32(&sdp_full), su32(&s_read), su32(&ds_full), su32(&dq_full),
+                   su32(&dq_read), it.it_end - it.it_begin);
+#endif
         mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
         mbar_init(&dq_read, 8);
@@ -461,7 +521,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const unsigned tmem = tmem_base;
     const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;  // dQ_n reuses T_DP
 
-    if (warp == 0) {
+    if (warp < 4) {
+#ifndef ODC_NO_SETMAXNREG
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+#endif
+      if (warp == 0) {
         if (lane == 0) {  // ---- TMA
             const int k0 = it.seq_start + j * BKV;
             mbar_expect_tx(&kv_full, 2 * kTile);
@@ -487,17 +551,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const unsigned id_kk = instr(0, 0), id_mm = instr(1, 1), id_km = instr(0, 1);
             mbar_wait(&kv_full, 0);
             const unsigned doa = su32(sdO), ka = su32(sK), va = su32(sV), pa = su32(sP), dsa = su32(sdS);
-            for (int n = 0; n < n_iter; ++n) {
+            auto issue_s = [&](int n) {  // S_n = Q_n K^T
                 const int b = n & 1;
                 const unsigned qa = su32(sQ0 + b * kTile);
                 mbar_wait(&q_full[b], (n >> 1) & 1);
-                // S columns were consumed by the elementwise warps (n-1) before their ds_full (waited below at n-1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {  // S = Q K^T (overlaps the dQ_{n-1} read-out)
+                for (int kk = 0; kk < HD / 16; ++kk) {
                     const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_S, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_kk, kk > 0);
                 }
+            };
+            issue_s(0);
+            for (int n = 0; n < n_iter; ++n) {
+                const int b = n & 1;
+                const unsigned qa = su32(sQ0 + b * kTile);
                 if (n > 0) mbar_wait(&dq_read, (n - 1) & 1);  // dP columns free again
                 mbar_wait(&do_full, n & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -507,7 +575,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma(tmem + T_DP, sdesc(doa + off, 16, 1024), sdesc(va + off, 16, 1024), id_kk, kk > 0);
                 }
                 commit(&sdp_full);
-                mbar_wait(&ds_full, n & 1);  // P, dS in smem; S, dP read
+#ifndef ODC_NO_EARLY_S
+                if (n + 1 < n_iter) {  // S_{n+1} overlaps the elementwise work of n once S_n is in registers
+                    mbar_wait(&s_read, n & 1);
+                    issue_s(n + 1);
+                }
+#endif
+                mbar_wait(&ds_full, n & 1);  // P, dS in smem
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk)  // K = query rows: MN-major A (P^T) and B (dO)
@@ -525,22 +599,42 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
                 }
                 commit(&dq_full);  // also: P, dS consumed
+#ifdef ODC_NO_EARLY_S
+                if (n + 1 < n_iter) issue_s(n + 1);
+#endif
             }
         }
-    } else {  // ---- elementwise / dQ / dK dV epilogue (warps 2..9): row quadrant warp%4, column half (warp-2)/4
+      }
+    } else {  // ---- elementwise / dQ / dK dV epilogue: row quadrant warp%4, column half
+#ifndef ODC_NO_SETMAXNREG
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+#endif
+#ifdef ODC_ATTN_DEBUG
+        if (lane == 0 && blockIdx.x == 0) printf("ew warp %d start\n", warp);
+#endif
         const int quad = warp % 4;
-        const int c0 = ((warp - 2) >> 2) * 64;  // this warp's 64 columns
-        const bool lead = warp == 2 && lane == 0;  // issues the TMA reductions
+        const int c0 = ((warp - 4) >> 2) * 64;  // this warp's 64 columns
+        const bool lead = warp == 4 && lane == 0;  // issues the TMA reductions
         const int r = quad * 32 + lane;  // row: query within tile i (loop) / key within tile j (epilogue)
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
         const float sl2 = g.scale_log2, sc = g.scale;
+        auto stats = [&](int n, float& lse_raw, float& d_raw) {  // row statistics of iteration n (prefetched)
+            const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
+            const int qi = i * BQ + r;
+            const long long idx = static_cast<long long>(h) * g.T + it.seq_start + qi;
+            const bool ok = n < n_iter && qi < it.seq_len;
+            lse_raw = ok ? __ldg(g.lse + idx) : 0.f;
+            d_raw = ok ? __ldg(g.D + idx) : 0.f;
+        };
+        float lse_nx, d_nx;
+        stats(0, lse_nx, d_nx);
         for (int n = 0; n < n_iter; ++n) {
             const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
             const int qi = i * BQ + r;  // query index within the sequence
             const bool q_ok = qi < it.seq_len;
-            const long long tok = static_cast<long long>(it.seq_start) + qi;
-            const float lse2 = q_ok ? g.lse[static_cast<long long>(h) * g.T + tok] * kLog2e : 0.f;
-            const float Ds = q_ok ? g.D[static_cast<long long>(h) * g.T + tok] * sc : 0.f;
+            const float lse2 = lse_nx * kLog2e;
+            const float Ds = d_nx * sc;
+            stats(n + 1, lse_nx, d_nx);
             const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV - c0 : -1;  // visible keys among our columns
             mbar_wait(&sdp_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -550,18 +644,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             TM_LD32(tmem + lane_base + T_DP + c0, dp);
             TM_LD32(tmem + lane_base + T_DP + c0 + 32, (dp + 32));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            // P = exp2(S*scale*log2e - lse2) (0 where masked), dS = P * (dP*scale - D*scale), packed bf16 in place
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_read);
+#ifdef ODC_ATTN_DEBUG
+            if (lane == 0 && blockIdx.x == 0) printf("ew warp %d n %d s_read\n", warp, n);
+#endif
+            // P = exp2(S*scale*log2e - lse2) (0 where masked), dS = P * (dP*scale - D*scale), packed bf16 in
+            // place; packed fp32x2 math, and no mask work on tiles this row sees entirely
+            const float2 v_sl2 = make_float2(sl2, sl2), v_nlse = make_float2(-lse2, -lse2);
+            const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
+            if (lim >= 63) {
 #pragma unroll
-            for (int x = 0; x < 64; x += 2) {
-                float p0 = ex2(fmaf(__uint_as_float(sv[x]), sl2, -lse2));
-                float p1 = ex2(fmaf(__uint_as_float(sv[x + 1]), sl2, -lse2));
-                if (x > lim) p0 = 0.f;
-                if (x + 1 > lim) p1 = 0.f;
-                const float d0 = p0 * fmaf(__uint_as_float(dp[x]), sc, -Ds);
-                const float d1 = p1 * fmaf(__uint_as_float(dp[x + 1]), sc, -Ds);
-                __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
-                sv[x / 2] = *reinterpret_cast<unsigned*>(&hp);
-                dp[x / 2] = *reinterpret_cast<unsigned*>(&hd);
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
+                    const float2 pp = make_float2(ex2(t.x), ex2(t.y));
+                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
+                    const float2 d = fmul2(pp, u);
+                    sv[x / 2] = pack_bf16(pp.x, pp.y);
+                    dp[x / 2] = pack_bf16(d.x, d.y);
+                }
+            } else {
+#pragma unroll
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
+                    const float2 pp = make_float2(x > lim ? 0.f : ex2(t.x), x + 1 > lim ? 0.f : ex2(t.y));
+                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
+                    const float2 d = fmul2(pp, u);
+                    sv[x / 2] = pack_bf16(pp.x, pp.y);
+                    dp[x / 2] = pack_bf16(d.x, d.y);
+                }
             }
             if (n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
                 if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
