@@ -1,21 +1,26 @@
-// attention.cu — causal varlen flash-attention FORWARD on tcgen05 (the
-// worker's attention; no reference counterpart — the reference models its
-// cost as alpha*s^2, src/cost_model.cpp:14-18). head_dim 128, bf16 in/out,
-// fp32 softmax statistics, GQA (H query heads share H/KV kv heads).
+// attention.cu — causal varlen flash-attention on tcgen05 (the worker's
+// attention; no reference counterpart — the reference models its cost as
+// alpha*s^2, src/cost_model.cpp:14-18). head_dim 128, bf16 in/out, fp32
+// softmax statistics, GQA (H query heads share H/KV kv heads).
 //
-// One CTA per (sequence, 128-query tile, query head), heaviest items first.
-//   warp 0     TMA: Q tile once; K_j / V_j tiles through a 2-stage ring.
-//              K and V use the same box {64 hd, 128 keys}: K is read as a
-//              K-major B operand (S = Q K^T), V as an MN-major B (O += P V).
-//   warp 1     single-thread tcgen05.mma issuer: S_{j+1} = Q K_{j+1}^T into
-//              the other TMEM S buffer while the softmax warps work on S_j,
-//              then O += P_j V_j (O accumulates in TMEM).
-//   warps 2-5  softmax, one query row per thread: tcgen05.ld S, causal /
-//              sequence-end mask, online max/sum in the exp2 domain with lazy
-//              rescaling (O is rescaled in TMEM only when the running max grows
-//              by more than 2^8), P (bf16) written to smem in the 128B-swizzled
-//              K-major layout the MMA reads; finally O / l -> bf16, and LSE.
-// TMEM: S0 [0,128) S1 [128,256) O [256,384) of 512 columns.
+// FORWARD. One CTA per (sequence, 256-query tile, query head), heaviest
+// items first. The 256 queries are two 128-row tiles Q0, Q1 that ping-pong on
+// the tensor core: while the softmax warpgroup of one tile works, the MMA
+// warp runs the other tile's MMAs, so each softmax hides behind 1024 clk of
+// tensor work.
+//   warp 0     TMA: Q0, Q1 once; K_j and V_j through separate 2-stage rings.
+//   warp 1     single-thread tcgen05.mma issuer, per KV tile j:
+//                PV0_{j-1}.. order: S0_j, S1_j, then O0 += P0_j V_j, S0_{j+1},
+//                O1 += P1_j V_j, S1_{j+1}.  P_t is read from TMEM (the A
+//                operand of a TS-MMA), V from smem.
+//   warps 4-7  softmax of Q0, warps 8-11 softmax of Q1 (setmaxnreg gives them
+//              the registers of warpgroup 0): one query row per thread,
+//              tcgen05.ld of the S row, causal / sequence-end mask, online
+//              max / sum in the exp2 domain with lazy rescaling (O_t is
+//              rescaled in TMEM only when the running max grows by more than
+//              2^8), P_t (bf16 pairs) stored with tcgen05.st over the first 64
+//              columns of S_t; finally O_t / l -> bf16, and the LSE.
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -35,9 +40,7 @@ namespace attn {
 
 constexpr int HD = 128;
 constexpr int BQ = 128, BKV = 128;
-constexpr int kThreads = 192;
 constexpr int kTile = BQ * HD * 2;              // 32 KB: one 128 x 128 bf16 tile (two 16 KB swizzle halves)
-constexpr int kSmem = kTile * 6 + 1024;         // Q, K x2, V x2, P
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;       // log2 units
 
@@ -181,34 +184,50 @@ struct Args {
     long long T;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kFwdThreads = 384;
+constexpr int BQ2 = 2 * BQ;                       // queries per forward CTA
+constexpr int kFwdSmem = kTile * 6 + 1024;         // Q0, Q1, K x2, V x2
+
+// bf16 x bf16 -> f32, M=128, N=128, A (P) from TMEM (K-major), B (V) MN-major
+__device__ __forceinline__ void mma_ts(unsigned d, unsigned a_tmem, std::uint64_t b, unsigned id, unsigned acc) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, Args g) {
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    char* sQ = smem;
-    char* sK[2] = {smem + kTile, smem + 2 * kTile};
-    char* sV[2] = {smem + 3 * kTile, smem + 4 * kTile};
-    char* sP = smem + 5 * kTile;
-    __shared__ __align__(8) unsigned long long q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, pv_done;
+    char* sQ = smem;               // Q0 | Q1
+    char* sK = smem + 2 * kTile;   // stage s at sK + s * kTile
+    char* sV = smem + 4 * kTile;
+    __shared__ __align__(8) unsigned long long q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2],
+        p_full[2], o_done[2];
     __shared__ unsigned tmem_base;
 
     const Item it = g.items[blockIdx.x];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int kvh = it.head / (g.H / g.KV);
-    const int q0 = it.q_tile * BQ;                        // first query row within the sequence
-    const int n_kv = min((it.seq_len + BKV - 1) / BKV, it.q_tile + 1);  // causal: keys <= last query
+    const int q0 = it.q_tile * BQ2;  // first query row within the sequence
+    const int n_kv_seq = (it.seq_len + BKV - 1) / BKV;
+    // causal: Q tile t (rows q0 + 128t ..) sees KV tiles 0 .. 2*q_tile + t
+    const int n0 = min(n_kv_seq, 2 * it.q_tile + 1), n1 = min(n_kv_seq, 2 * it.q_tile + 2);
 
     if (warp == 0 && lane == 0) {
         mbar_init(&q_full, 1);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
             mbar_init(&s_full[s], 1);
-            mbar_init(&s_free[s], 4);
+            mbar_init(&p_full[s], 4);
+            mbar_init(&o_done[s], 1);
         }
-        mbar_init(&p_full, 4);
-        mbar_init(&pv_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_q) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
@@ -224,135 +243,145 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const unsigned tmem = tmem_base;
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---- TMA
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
+        if (warp == 0 && lane == 0) {  // ---- TMA
             const int row0 = it.seq_start + q0;
-            mbar_expect_tx(&q_full, kTile);
+            mbar_expect_tx(&q_full, 2 * kTile);
             tma_2d(&map_q, &q_full, sQ, it.head * HD, row0);
             tma_2d(&map_q, &q_full, sQ + kTile / 2, it.head * HD + 64, row0);
-            for (int j = 0; j < n_kv; ++j) {
-                const int s = j & 1;
-                if (j >= 2) mbar_wait(&kv_empty[s], ((j >> 1) - 1) & 1);
-                const int k0 = it.seq_start + j * BKV;
-                mbar_expect_tx(&kv_full[s], 2 * kTile);
-                tma_2d(&map_k, &kv_full[s], sK[s], kvh * HD, k0);
-                tma_2d(&map_k, &kv_full[s], sK[s] + kTile / 2, kvh * HD + 64, k0);
-                tma_2d(&map_v, &kv_full[s], sV[s], kvh * HD, k0);
-                tma_2d(&map_v, &kv_full[s], sV[s] + kTile / 2, kvh * HD + 64, k0);
+            tma_2d(&map_q, &q_full, sQ + kTile, it.head * HD, row0 + BQ);
+            tma_2d(&map_q, &q_full, sQ + kTile + kTile / 2, it.head * HD + 64, row0 + BQ);
+            for (int j = 0; j < n1; ++j) {
+                const int s = j & 1, k0 = it.seq_start + j * BKV;
+                if (j >= 2) mbar_wait(&k_empty[s], ((j >> 1) - 1) & 1);
+                mbar_expect_tx(&k_full[s], kTile);
+                tma_2d(&map_k, &k_full[s], sK + s * kTile, kvh * HD, k0);
+                tma_2d(&map_k, &k_full[s], sK + s * kTile + kTile / 2, kvh * HD + 64, k0);
+                if (j >= 2) mbar_wait(&v_empty[s], ((j >> 1) - 1) & 1);
+                mbar_expect_tx(&v_full[s], kTile);
+                tma_2d(&map_v, &v_full[s], sV + s * kTile, kvh * HD, k0);
+                tma_2d(&map_v, &v_full[s], sV + s * kTile + kTile / 2, kvh * HD + 64, k0);
             }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
+        } else if (warp == 1 && lane == 0) {  // ---- MMA issuer
             const unsigned id_qk = idesc(0), id_pv = idesc(1);
             mbar_wait(&q_full, 0);
-            auto issue_s = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&kv_full[s], (j >> 1) & 1);
-                if (j >= 2) mbar_wait(&s_free[s], ((j >> 1) - 1) & 1);  // softmax finished reading S_{j-2}
+            auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T into TMEM columns [128t, 128t + 128)
+                const unsigned qa = su32(sQ + t * kTile), ka = su32(sK + (j & 1) * kTile);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const unsigned qa = su32(sQ), ka = su32(sK[s]);
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {  // K dim = head dim, two 64-wide swizzle halves
+                for (int kk = 0; kk < HD / 16; ++kk) {
                     const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                    mma(tmem + s * 128, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_qk, kk > 0);
+                    mma(tmem + t * 128, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_qk, kk > 0);
                 }
-                commit(&s_full[s]);
+                commit(&s_full[t]);
             };
-            issue_s(0);
-            for (int j = 0; j < n_kv; ++j) {
-                if (j + 1 < n_kv) issue_s(j + 1);
-                mbar_wait(&p_full, j & 1);  // P_j in smem (and O rescaled)
+            auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, P_t = bf16 pairs in TMEM columns [128t, 128t + 64)
+                const unsigned va = su32(sV + (j & 1) * kTile);
+                mbar_wait(&p_full[t], j & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc(va + kk * 2048, kTile / 2, 1024), id_pv,
+                           (j > 0 || kk > 0));
+            };
+            mbar_wait(&k_full[0], 0);
+            issue_s(0, 0);
+            issue_s(1, 0);
+            commit(&k_empty[0]);
+            for (int j = 0; j < n1; ++j) {
                 const int s = j & 1;
-                const unsigned pa = su32(sP), va = su32(sV[s]);
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {  // K dim = keys
-                    const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;  // P: K-major
-                    const unsigned boff = kk * 2048;                                // V: MN-major, 16 key rows
-                    mma(tmem + 256, sdesc(pa + aoff, 16, 1024), sdesc(va + boff, kTile / 2, 1024), id_pv, (j > 0 || kk > 0));
+                mbar_wait(&v_full[s], (j >> 1) & 1);
+                if (j < n0) issue_pv(0, j);
+                if (j + 1 == n0) commit(&o_done[0]);
+                const bool more = j + 1 < n1;
+                if (more) mbar_wait(&k_full[s ^ 1], ((j + 1) >> 1) & 1);
+                if (j + 1 < n0) issue_s(0, j + 1);
+                issue_pv(1, j);
+                commit(&v_empty[s]);
+                if (more) {
+                    issue_s(1, j + 1);
+                    commit(&k_empty[s ^ 1]);
                 }
-                commit(&kv_empty[s]);  // K_j, V_j consumed
-                commit(&pv_done);      // P buffer free, O stable
             }
+            commit(&o_done[1]);
         }
-    } else {  // ---- softmax / correction / epilogue (warps 2..5)
+    } else {  // ---- softmax / correction / epilogue: warpgroup t = Q tile t
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+        const int t = (warp - 4) >> 2;
         const int quad = warp % 4;
-        const int r = quad * 32 + lane;  // query row within the tile
-        const int qi = q0 + r;           // query index within the sequence
+        const int r = quad * 32 + lane;          // query row within tile t
+        const int qi = q0 + t * BQ + r;          // query index within the sequence
+        const int n_t = t ? n1 : n0;
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
-        float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < n_kv; ++j) {
-            const int s = j & 1;
-            mbar_wait(&s_full[s], (j >> 1) & 1);
+        const unsigned t_s = tmem + lane_base + t * 128, t_o = tmem + lane_base + 256 + t * 128;
+        const float sl2 = g.scale_log2;
+        float m = -INFINITY, l0 = 0.f, l1 = 0.f;  // running max (scaled, log2 units), two partial row sums
+        for (int j = 0; j < n_t; ++j) {
+            mbar_wait(&s_full[t], j & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            // the whole S row in registers: 4 TMEM loads in flight, one wait
             unsigned v[128];
-            TM_LD32(tmem + lane_base + s * 128 + 0, (v + 0));
-            TM_LD32(tmem + lane_base + s * 128 + 32, (v + 32));
-            TM_LD32(tmem + lane_base + s * 128 + 64, (v + 64));
-            TM_LD32(tmem + lane_base + s * 128 + 96, (v + 96));
+            TM_LD32(t_s + 0, (v + 0));
+            TM_LD32(t_s + 32, (v + 32));
+            TM_LD32(t_s + 64, (v + 64));
+            TM_LD32(t_s + 96, (v + 96));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_free[s]);  // S buffer reusable for S_{j+2}
-            const int kbase = j * BKV;
             // keys e <= lim are visible to this query (causal + sequence end)
-            const int lim = min(qi, it.seq_len - 1) - kbase;
+            const int lim = min(qi, it.seq_len - 1) - j * BKV;
             float mx = -INFINITY;
+            if (lim >= BKV - 1) {
 #pragma unroll
-            for (int e = 0; e < 128; ++e) {
-                const float x = __uint_as_float(v[e]) * g.scale_log2;
-                v[e] = __float_as_uint(e <= lim ? x : -INFINITY);
-                mx = fmaxf(mx, __uint_as_float(v[e]));
+                for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 128; ++e) {
+                    if (e > lim) v[e] = __float_as_uint(-INFINITY);
+                    mx = fmaxf(mx, __uint_as_float(v[e]));
+                }
             }
+            mx *= sl2;  // scale > 0: max commutes with the scaling
             float m_new = m;
             if (mx > m + kRescaleThreshold || m == -INFINITY) m_new = fmaxf(mx, m);
-            // P_{j-1} consumed and O_{j-1} complete before we touch P / O
-            if (j > 0) mbar_wait(&pv_done, (j - 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (j > 0 && m_new != m) {  // lazy rescale of the running output in TMEM
+            if (j > 0 && m_new != m) {  // lazy rescale of O_t (PV_t of j-1 completed before S_t of j)
                 const float alpha = ex2(m - m_new);
-                l *= alpha;
+                l0 *= alpha;
+                l1 *= alpha;
 #pragma unroll 1
-                for (int c = 0; c < HD; c += 32) {  // chunked: S row stays in registers
+                for (int c = 0; c < HD; c += 32) {
                     unsigned o[32];
-                    TM_LD32(tmem + lane_base + 256 + c, o);
+                    TM_LD32(t_o + c, o);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                     for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    TM_ST32(tmem + lane_base + 256 + c, o);
+                    TM_ST32(t_o + c, o);
                 }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             m = m_new;
             const float mm = (m == -INFINITY) ? 0.f : m;
-            // p = exp2(x - m) -> bf16 P in smem (128B-swizzled K-major), row sum of what the MMA sees
+            // p = exp2(s*scale*log2e - m) -> bf16 pairs, packed in place into v[0..63]
+            const float2 v_sl2 = make_float2(sl2, sl2), v_nm = make_float2(-mm, -mm);
+            float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < BKV; c += 32) {
-                unsigned pk[16];
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const float p0 = ex2(__uint_as_float(v[c + e]) - mm);
-                    const float p1 = ex2(__uint_as_float(v[c + e + 1]) - mm);
-                    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-                    l += __low2float(h) + __high2float(h);
-                    pk[e / 2] = *reinterpret_cast<unsigned*>(&h);
-                }
-                char* half = sP + (c >> 6) * (kTile / 2) + r * 128;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int chunk = ((c & 63) >> 3) + q;
-                    sts128(half + ((chunk ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                }
+            for (int e = 0; e < 128; e += 2) {
+                const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), v_sl2, v_nm);
+                const float p0 = ex2(x.x), p1 = ex2(x.y);
+                acc.x += p0;
+                acc.y += p1;
+                v[e / 2] = pack_bf16(p0, p1);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+            l0 += acc.x;
+            l1 += acc.y;
+            TM_ST32(t_s + 0, (v + 0));
+            TM_ST32(t_s + 32, (v + 32));
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full);
+            if (lane == 0) mbar_arrive(&p_full[t]);
         }
-        // epilogue: O / l -> bf16, LSE
-        mbar_wait(&pv_done, (n_kv - 1) & 1);
+        // epilogue: O_t / l -> bf16, LSE
+        mbar_wait(&o_done[t], 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const float l = l0 + l1;
         const bool valid = qi < it.seq_len;
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const long long tok = static_cast<long long>(it.seq_start) + qi;
@@ -360,19 +389,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int c = 0; c < HD; c += 32) {
             unsigned v[32];
-            TM_LD32(tmem + lane_base + 256 + c, v);
+            TM_LD32(t_o + c, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (valid) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint4 o;
-                    unsigned* w = reinterpret_cast<unsigned*>(&o);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * q + 2 * e]) * inv,
-                                                                 __uint_as_float(v[8 * q + 2 * e + 1]) * inv);
-                        w[e] = *reinterpret_cast<unsigned*>(&h);
-                    }
+                    o.x = pack_bf16(__uint_as_float(v[8 * q]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+                    o.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+                    o.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+                    o.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
                     *reinterpret_cast<uint4*>(orow + c + 8 * q) = o;
                 }
             }
@@ -654,6 +680,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // place; packed fp32x2 math, and no mask work on tiles this row sees entirely
             const float2 v_sl2 = make_float2(sl2, sl2), v_nlse = make_float2(-lse2, -lse2);
             const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
+#ifdef ODC_EXP_NO_E
+            if (true) {
+#pragma unroll
+                for (int x = 0; x < 64; x += 2) {
+                    sv[x / 2] = sv[x] ^ sv[x + 1];
+                    dp[x / 2] = dp[x] ^ dp[x + 1];
+                }
+            } else
+#endif
             if (lim >= 63) {
 #pragma unroll
                 for (int x = 0; x < 64; x += 2) {
@@ -675,10 +710,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     dp[x / 2] = pack_bf16(d.x, d.y);
                 }
             }
+#ifndef ODC_EXP_NO_DQ_WAIT
             if (n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
                 if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 bar_ew();
             }
+#endif
             store_swizzled(sP, r, c0, sv);
             store_swizzled(sP, r, c0 + 32, sv + 16);
             store_swizzled(sdS, r, c0, dp);
@@ -691,6 +728,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef ODC_EXP_NO_DQ
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dq_read);
+            continue;
+#endif
             unsigned v[64];
             TM_LD32(tmem + lane_base + T_DP + c0, v);
             TM_LD32(tmem + lane_base + T_DP + c0 + 32, (v + 32));
@@ -704,7 +746,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             if (lead) {
                 const int row0 = it.seq_start + i * BQ;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
+                for (int k = 0; k < 4; ++k) {
+#if defined(ODC_EXP_DQ_STORE)
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                     &map_dq),
+                                 "r"(h * HD + 32 * k), "r"(row0), "r"(su32(stage + k * (kTile / 2)))
+                                 : "memory");
+#elif defined(ODC_EXP_DQ_HALF)
+                    if (k < 2) tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
+#elif !defined(ODC_EXP_NO_DQ_TMA)
+                    tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
+#endif
+                }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
@@ -836,7 +889,7 @@ extern "C" odc_status odc_attn_fwd(const void* q, const void* k, const void* v, 
         int dev = 0;
         cudaGetDevice(&dev);
         if (configured != dev) {
-            cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
             if (e != cudaSuccess) throw std::runtime_error(std::string("attn smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
@@ -854,7 +907,7 @@ extern "C" odc_status odc_attn_fwd(const void* q, const void* k, const void* v, 
         a.lse = lse;
         a.T = T;
         odc::count_launch();
-        attn_fwd_kernel<<<n_items, kThreads, kSmem, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, a);
+        attn_fwd_kernel<<<n_items, kFwdThreads, kFwdSmem, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, a);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw std::runtime_error(std::string("attn_fwd launch: ") + cudaGetErrorString(e));
     });

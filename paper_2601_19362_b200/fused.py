@@ -83,10 +83,11 @@ def ce_fwd_bwd_(logits, labels, scale, loss_accum):
 
 def attn_items(lens, H: int, device) -> torch.Tensor:
     """Work list of the tcgen05 attention forward: one item per (sequence,
-    128-query tile, head), heaviest (most causal KV tiles) first."""
+    256-query tile = two 128-row tiles, head), heaviest (most causal KV tiles)
+    first."""
     items, start = [], 0
     for n in lens:
-        for qt in range((n + 127) // 128):
+        for qt in range((n + 255) // 256):
             for h in range(H):
                 items.append((start, n, qt, h))
         start += n
