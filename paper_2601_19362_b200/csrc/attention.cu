@@ -138,6 +138,35 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
 }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nadd.rn.f32x2 rd, ra, rb;\n"
+        "mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+// 2^x on the FMA pipe (takes load off MUFU.EX2): round-to-nearest split x = j + f via the 1.5*2^23 trick,
+// degree-3 minimax of 2^f on [-0.5, 0.5] (max rel. error 7.5e-5, far below the bf16 rounding of P), then j
+// added to the exponent field. x is clamped at -125 (masked scores give ~2^-125 instead of 0).
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+    x.x = fmaxf(x.x, -125.f);  // keeps the exponent field of the result >= 1 (2^f >= 0.707 has exponent 126)
+    x.y = fmaxf(x.y, -125.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = fadd2(x, magic);
+    const float2 jf = fadd2(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = fadd2(x, make_float2(-jf.x, -jf.y));
+    float2 p = ffma2(f, make_float2(0.05517132f, 0.05517132f), make_float2(0.24261054f, 0.24261054f));
+    p = ffma2(p, f, make_float2(0.69326099f, 0.69326099f));
+    p = ffma2(p, f, make_float2(0.99992811f, 0.99992811f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ unsigned pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<unsigned*>(&h);
@@ -328,17 +357,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             // keys e <= lim are visible to this query (causal + sequence end)
             const int lim = min(qi, it.seq_len - 1) - j * BKV;
-            float mx = -INFINITY;
-            if (lim >= BKV - 1) {
+            if (lim < BKV - 1) {
 #pragma unroll
-                for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
-            } else {
-#pragma unroll
-                for (int e = 0; e < 128; ++e) {
+                for (int e = 0; e < 128; ++e)
                     if (e > lim) v[e] = __float_as_uint(-INFINITY);
-                    mx = fmaxf(mx, __uint_as_float(v[e]));
-                }
             }
+            // row max: 8 independent chains of 3-input max (short dependency chains)
+            float mxa[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mxa[k] = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 128; e += 16) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    mxa[k] = fmax3(mxa[k], __uint_as_float(v[e + 2 * k]), __uint_as_float(v[e + 2 * k + 1]));
+            }
+            float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]));
             mx *= sl2;  // scale > 0: max commutes with the scaling
             float m_new = m;
             if (mx > m + kRescaleThreshold || m == -INFINITY) m_new = fmaxf(mx, m);
@@ -359,18 +393,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             m = m_new;
             const float mm = (m == -INFINITY) ? 0.f : m;
             // p = exp2(s*scale*log2e - m) -> bf16 pairs, packed in place into v[0..63]
+            // one pair in four goes through the FMA-pipe exp2 so MUFU is not the bottleneck
             const float2 v_sl2 = make_float2(sl2, sl2), v_nm = make_float2(-mm, -mm);
-            float2 acc = make_float2(0.f, 0.f);
+            float2 acc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int e = 0; e < 128; e += 2) {
                 const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), v_sl2, v_nm);
-                const float p0 = ex2(x.x), p1 = ex2(x.y);
-                acc.x += p0;
-                acc.y += p1;
-                v[e / 2] = pack_bf16(p0, p1);
+#ifndef ODC_NO_EX2_EMU
+                const float2 p = ((e >> 1) & 3) == 3 ? ex2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
+#else
+                const float2 p = make_float2(ex2(x.x), ex2(x.y));
+#endif
+                acc[(e >> 1) & 3] = fadd2(acc[(e >> 1) & 3], p);
+                v[e / 2] = pack_bf16(p.x, p.y);
             }
-            l0 += acc.x;
-            l1 += acc.y;
+            const float2 acc01 = fadd2(acc[0], acc[1]), acc23 = fadd2(acc[2], acc[3]);
+            l0 += acc01.x + acc23.x;
+            l1 += acc01.y + acc23.y;
             TM_ST32(t_s + 0, (v + 0));
             TM_ST32(t_s + 32, (v + 32));
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
