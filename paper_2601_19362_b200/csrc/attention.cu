@@ -401,11 +401,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
             for (int e = 0; e < 128; e += 2) {
                 const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), v_sl2, v_nm);
-#ifndef ODC_NO_EX2_EMU
                 const float2 p = ((e >> 1) & 3) == 3 ? ex2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
-#else
-                const float2 p = make_float2(ex2(x.x), ex2(x.y));
-#endif
                 acc[(e >> 1) & 3] = fadd2(acc[(e >> 1) & 3], p);
                 v[e / 2] = pack_bf16(p.x, p.y);
             }
@@ -589,9 +585,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;  // dQ_n reuses T_DP
 
     if (warp < 4) {
-#ifndef ODC_NO_SETMAXNREG
       asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
-#endif
       if (warp == 0) {
         if (lane == 0) {  // ---- TMA
             const int k0 = it.seq_start + j * BKV;
@@ -642,12 +636,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma(tmem + T_DP, sdesc(doa + off, 16, 1024), sdesc(va + off, 16, 1024), id_kk, kk > 0);
                 }
                 commit(&sdp_full);
-#ifndef ODC_NO_EARLY_S
                 if (n + 1 < n_iter) {  // S_{n+1} overlaps the elementwise work of n once S_n is in registers
                     mbar_wait(&s_read, n & 1);
                     issue_s(n + 1);
                 }
-#endif
                 mbar_wait(&ds_full, n & 1);  // P, dS in smem
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
@@ -666,16 +658,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
                 }
                 commit(&dq_full);  // also: P, dS consumed
-#ifdef ODC_NO_EARLY_S
-                if (n + 1 < n_iter) issue_s(n + 1);
-#endif
             }
         }
       }
     } else {  // ---- elementwise / dQ / dK dV epilogue: row quadrant warp%4, column half
-#ifndef ODC_NO_SETMAXNREG
         asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
-#endif
 #ifdef ODC_ATTN_DEBUG
         if (lane == 0 && blockIdx.x == 0) printf("ew warp %d start\n", warp);
 #endif
@@ -721,15 +708,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // place; packed fp32x2 math, and no mask work on tiles this row sees entirely
             const float2 v_sl2 = make_float2(sl2, sl2), v_nlse = make_float2(-lse2, -lse2);
             const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
-#ifdef ODC_EXP_NO_E
-            if (true) {
-#pragma unroll
-                for (int x = 0; x < 64; x += 2) {
-                    sv[x / 2] = sv[x] ^ sv[x + 1];
-                    dp[x / 2] = dp[x] ^ dp[x + 1];
-                }
-            } else
-#endif
             if (lim >= 63) {
 #pragma unroll
                 for (int x = 0; x < 64; x += 2) {
@@ -751,12 +729,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     dp[x / 2] = pack_bf16(d.x, d.y);
                 }
             }
-#ifndef ODC_EXP_NO_DQ_WAIT
             if (n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
                 if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 bar_ew();
             }
-#endif
             store_swizzled(sP, r, c0, sv);
             store_swizzled(sP, r, c0 + 32, sv + 16);
             store_swizzled(sdS, r, c0, dp);
@@ -769,11 +745,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#ifdef ODC_EXP_NO_DQ
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&dq_read);
-            continue;
-#endif
             unsigned v[64];
             TM_LD32(tmem + lane_base + T_DP + c0, v);
             TM_LD32(tmem + lane_base + T_DP + c0 + 32, (v + 32));
@@ -788,16 +759,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const int row0 = it.seq_start + i * BQ;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-#if defined(ODC_EXP_DQ_STORE)
-                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                                     &map_dq),
-                                 "r"(h * HD + 32 * k), "r"(row0), "r"(su32(stage + k * (kTile / 2)))
-                                 : "memory");
-#elif defined(ODC_EXP_DQ_HALF)
-                    if (k < 2) tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
-#elif !defined(ODC_EXP_NO_DQ_TMA)
                     tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
-#endif
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
