@@ -42,19 +42,22 @@ class Shape:
         return self.nonembed_params / (self.layers * self.d)
 
     def beta_over_alpha_b200(self) -> float:
-        """FLOP ratio scaled by the measured B200 throughput ratio of the two
-        terms' kernels: the tcgen05 attention fwd+bwd ~500 TFLOP/s (fwd
-        500-755, bwd 437-513, profiles/r01) vs the tcgen05 GEMMs ~1,280
-        TFLOP/s in the step, i.e. an attention FLOP costs ~2.6x a dense FLOP. The cost
-        model's absolute scale is a free knob (inc/cost_model.hpp:10-12); only
-        beta/alpha shapes the plan, identically for ODC and FSDP."""
-        # the LM head (6*V*d per token, tcgen05 GEMM) is linear work too
+        """beta/alpha measured on B200: tools/calibrate_cost.py times one SFT
+        microbatch (fwd + bwd, this repo's kernels) for 15 length mixes and fits
+        t = alpha*sum(s^2) + beta*sum(s) + c (the reference's per-sample cost,
+        src/cost_model.cpp:14-18): beta/alpha = 26,685 for Qwen2.5-1.5B (max
+        residual 1.7%, profiles/r01/cost_calibration_qwen1.5b.jsonl). Expressed
+        as the FLOP ratio (linear work incl. the LM head, per layer-width) times
+        the measured attention-vs-linear cost factor, so other shapes scale by
+        their own FLOP ratio. The cost model's absolute scale is a free knob
+        (inc/cost_model.hpp:10-12); only beta/alpha shapes the plan, identically
+        for ODC and FSDP."""
         linear = (self.nonembed_params + self.vocab * self.d) / (self.layers * self.d)
-        return linear * (ATTN_TFLOPS / GEMM_TFLOPS)
+        return linear * B200_ATTN_VS_LINEAR
 
 
-ATTN_TFLOPS = 500.0
-GEMM_TFLOPS = 1280.0
+# measured: 26,685 / ((P_nonembed + V*d) / (L*d)) for Qwen2.5-1.5B on B200
+B200_ATTN_VS_LINEAR = 0.7433
 
 QWEN25_1_5B = Shape("qwen2.5-1.5b", 1536, 8960, 28, 12, 2, 151936, True, True)
 LLAMA3_8B = Shape("llama-3-8b", 4096, 14336, 32, 32, 8, 128256, False, False)
