@@ -113,6 +113,84 @@ __global__ void rmsnorm_bwd_kernel(const uint4* __restrict__ dy, const uint4* __
     for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(&dw[i], sdw[i]);
 }
 
+// Register-accumulator variant: lane l of every warp owns the uint4 columns l, l+32, .. (KMAX per lane), so
+// the dw partial of the rows a warp handles stays in registers; one shared-memory reduction per block at the end.
+template <int KMAX>
+__global__ void __launch_bounds__(256, 2) rmsnorm_bwd_reg_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
+                                                                const uint4* __restrict__ w, const float* __restrict__ rstd,
+                                                                const uint4* __restrict__ resid, uint4* __restrict__ out,
+                                                                float* __restrict__ dw, long long T, int dv) {
+    extern __shared__ float sdw[];
+    const int d = dv * 8;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) sdw[i] = 0.f;
+    const int lane = threadIdx.x % 32, wid = threadIdx.x / 32, nw = blockDim.x / 32;
+    float acc[KMAX][8];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[k][j] = 0.f;
+    }
+    for (long long row = static_cast<long long>(blockIdx.x) * nw + wid; row < T; row += static_cast<long long>(gridDim.x) * nw) {
+        const float r = rstd[row];
+        const uint4* dyr = dy + row * dv;
+        const uint4* xr = x + row * dv;
+        float dot = 0.f;
+        {  // pass 1: all loads of the row in flight, then the dot product
+            uint4 ra[KMAX], rb[KMAX];
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                const int i = lane + 32 * k;
+                if (i < dv) {
+                    ra[k] = dyr[i];
+                    rb[k] = xr[i];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                const int i = lane + 32 * k;
+                if (i < dv) {
+                    float a[8], bb[8], g[8];
+                    unpack8(ra[k], a);
+                    unpack8(rb[k], bb);
+                    unpack8(__ldg(w + i), g);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dot += a[j] * g[j] * bb[j];
+                }
+            }
+        }
+        const float c = warp_sum(dot) * r / d;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {  // pass 2: the row again (L1 hits), residual, output, dw partial
+            const int i = lane + 32 * k;
+            if (i < dv) {
+                float a[8], bb[8], g[8], o[8];
+                unpack8(dyr[i], a);
+                unpack8(xr[i], bb);
+                unpack8(__ldg(w + i), g);
+                if (resid) unpack8(resid[row * dv + i], o);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float xh = bb[j] * r;
+                    o[j] = (resid ? o[j] : 0.f) + r * (a[j] * g[j] - xh * c);
+                    acc[k][j] += a[j] * xh;  // dw += dy * xhat
+                }
+                out[row * dv + i] = pack8(o);
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int i = lane + 32 * k;
+        if (i < dv) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) atomicAdd(&sdw[i * 8 + j], acc[k][j]);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(&dw[i], sdw[i]);
+}
+
 // ------------------------------------------------------------------- RoPE
 // rotate-half convention: y1 = x1 c - x2 s, y2 = x2 c + x1 s (inverse: s -> -s)
 // table: [max_pos][hd/2] float2 {cos, sin}
@@ -217,40 +295,42 @@ __global__ void col_sum_kernel(const unsigned short* __restrict__ m, float* __re
 }
 
 // ----------------------------------------------------------------- SwiGLU
+// one row per block-iteration, columns across the threads: no 64-bit division per element
 __global__ void swiglu_fwd_kernel(const uint4* __restrict__ gu, uint4* __restrict__ m, long long T, int fv) {
-    const long long total = T * fv;
-    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long t = i / fv;
-        const int c = static_cast<int>(i % fv);
-        float g[8], u[8];
-        unpack8(gu[t * 2 * fv + c], g);
-        unpack8(gu[t * 2 * fv + fv + c], u);
+    for (long long t = blockIdx.x; t < T; t += gridDim.x) {
+        const uint4* gr = gu + t * 2 * fv;
+        uint4* mr = m + t * fv;
+        for (int c = threadIdx.x; c < fv; c += blockDim.x) {
+            float g[8], u[8];
+            unpack8(gr[c], g);
+            unpack8(gr[fv + c], u);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) g[j] = g[j] / (1.f + __expf(-g[j])) * u[j];
-        m[i] = pack8(g);
+            for (int j = 0; j < 8; ++j) g[j] = __fdividef(g[j], 1.f + __expf(-g[j])) * u[j];
+            mr[c] = pack8(g);
+        }
     }
 }
 
 __global__ void swiglu_bwd_kernel(const uint4* __restrict__ dm, const uint4* __restrict__ gu, uint4* __restrict__ dgu,
                                   long long T, int fv) {
-    const long long total = T * fv;
-    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long t = i / fv;
-        const int c = static_cast<int>(i % fv);
-        float d[8], g[8], u[8], dg[8], du[8];
-        unpack8(dm[i], d);
-        unpack8(gu[t * 2 * fv + c], g);
-        unpack8(gu[t * 2 * fv + fv + c], u);
+    for (long long t = blockIdx.x; t < T; t += gridDim.x) {
+        const uint4* gr = gu + t * 2 * fv;
+        const uint4* dr = dm + t * fv;
+        uint4* orow = dgu + t * 2 * fv;
+        for (int c = threadIdx.x; c < fv; c += blockDim.x) {
+            float d[8], g[8], u[8], dg[8], du[8];
+            unpack8(dr[c], d);
+            unpack8(gr[c], g);
+            unpack8(gr[fv + c], u);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float sg = 1.f / (1.f + __expf(-g[j]));
-            dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
-            du[j] = d[j] * g[j] * sg;
+            for (int j = 0; j < 8; ++j) {
+                const float sg = __frcp_rn(1.f + __expf(-g[j]));
+                dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
+                du[j] = d[j] * g[j] * sg;
+            }
+            orow[c] = pack8(dg);
+            orow[fv + c] = pack8(du);
         }
-        dgu[t * 2 * fv + c] = pack8(dg);
-        dgu[t * 2 * fv + fv + c] = pack8(du);
     }
 }
 
@@ -356,9 +436,23 @@ odc_status odc_w_rmsnorm_bwd(const void* dy, const void* x, const void* w, const
         need(d % 8 == 0, "rmsnorm: d % 8 == 0");
         const int blocks = static_cast<int>(std::min<long long>((T + 7) / 8, 148 * 4));
         odc::count_launch();
-        rmsnorm_bwd_kernel<<<blocks, 256, d * sizeof(float), reinterpret_cast<cudaStream_t>(stream)>>>(
-            static_cast<const uint4*>(dy), static_cast<const uint4*>(x), static_cast<const uint4*>(w), rstd,
-            static_cast<const uint4*>(resid), static_cast<uint4*>(out), dw, T, d / 8);
+        const int kmax = (d / 8 + 31) / 32;  // uint4 columns per lane
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        auto args = [&](auto kern) {
+            kern<<<blocks, 256, d * sizeof(float), st>>>(static_cast<const uint4*>(dy), static_cast<const uint4*>(x),
+                                                         static_cast<const uint4*>(w), rstd,
+                                                         static_cast<const uint4*>(resid), static_cast<uint4*>(out), dw,
+                                                         T, d / 8);
+        };
+        switch (kmax) {
+            case 1: args(rmsnorm_bwd_reg_kernel<1>); break;
+            case 2: args(rmsnorm_bwd_reg_kernel<2>); break;
+            case 3: args(rmsnorm_bwd_reg_kernel<3>); break;
+            case 4: args(rmsnorm_bwd_reg_kernel<4>); break;
+            case 5: args(rmsnorm_bwd_reg_kernel<5>); break;
+            case 6: args(rmsnorm_bwd_reg_kernel<6>); break;
+            default: args(rmsnorm_bwd_kernel); break;  // wide rows: shared-memory dw accumulation
+        }
         ok(cudaGetLastError(), "rmsnorm_bwd");
     });
 }
@@ -406,7 +500,8 @@ odc_status odc_w_swiglu_fwd(const void* gu, void* m, std::int64_t T, int ffn, vo
     return odc::guard([&] {
         need(ffn % 8 == 0, "swiglu: ffn % 8 == 0");
         odc::count_launch();
-        swiglu_fwd_kernel<<<grid_for(T * ffn / 8, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        swiglu_fwd_kernel<<<static_cast<unsigned>(std::min<long long>(T, 148 * 8)), 256, 0,
+                            reinterpret_cast<cudaStream_t>(stream)>>>(
             static_cast<const uint4*>(gu), static_cast<uint4*>(m), T, ffn / 8);
         ok(cudaGetLastError(), "swiglu_fwd");
     });
@@ -416,7 +511,8 @@ odc_status odc_w_swiglu_bwd(const void* dm, const void* gu, void* dgu, std::int6
     return odc::guard([&] {
         need(ffn % 8 == 0, "swiglu: ffn % 8 == 0");
         odc::count_launch();
-        swiglu_bwd_kernel<<<grid_for(T * ffn / 8, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        swiglu_bwd_kernel<<<static_cast<unsigned>(std::min<long long>(T, 148 * 8)), 256, 0,
+                            reinterpret_cast<cudaStream_t>(stream)>>>(
             static_cast<const uint4*>(dm), static_cast<const uint4*>(gu), static_cast<uint4*>(dgu), T, ffn / 8);
         ok(cudaGetLastError(), "swiglu_bwd");
     });

@@ -18,7 +18,7 @@ def bf(*s, scale=1.0):
     return (torch.randn(*s, device=DEV) * scale).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("T,d", [(5, 256), (1000, 1536), (77, 4096)])
+@pytest.mark.parametrize("T,d", [(5, 256), (1000, 1536), (64, 2048), (77, 4096), (3, 5120)])
 def test_rmsnorm(T, d):
     x, w, dy, res = bf(T, d), bf(d, scale=0.3) + 1, bf(T, d), bf(T, d)
     y, rstd = F.rmsnorm_fwd(x, w)

@@ -16,7 +16,7 @@ shape = SHAPES[os.environ.get("MODEL", "qwen2.5-1.5b")]
 dev = torch.device("cuda", 0)
 sizes = W.unit_sizes(shape)
 lens = [max(512, x) for x in P.generate_synthetic(("lognormal", 8.0, 1.5), 2048, 32768, 0)]
-plan = P.plan_flat("lb-mini", lens, 1, 8, 32768, P.CostModel(1.0, shape.beta_over_alpha(), 1))
+plan = P.plan_flat("lb-mini", lens, 1, 8, 32768, P.CostModel(1.0, shape.beta_over_alpha_b200(), 1))
 eng = OdcEngine(sizes)
 gen = torch.Generator(device=dev).manual_seed(0)
 for u in range(len(sizes)):
@@ -27,7 +27,7 @@ wk = W.Worker(shape, W.OdcComm(eng), dev)
 def step(k):
     tot = float(sum(lens[i] for dv in plan[k] for mb in dv for i in mb))
     for mb in plan[k][0]:
-        wk.microbatch(W.make_batch(lens, mb, shape.vocab, dev), sum(lens[i] for i in mb) / tot)
+        wk.microbatch(W.make_batch(lens, mb, shape.vocab, dev, heads=shape.heads, kv_heads=shape.kv_heads), sum(lens[i] for i in mb) / tot)
     wk.minibatch_end()
 
 
