@@ -224,6 +224,10 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
             c->dev();
             cuda_ok(cudaMalloc(&c->arena, static_cast<std::size_t>(off)), "cudaMalloc arena");
             cuda_ok(cudaMemset(c->arena, 0, static_cast<std::size_t>(off)), "memset arena");
+            // the zeroed flags page must be visible before the arena is exported: peers poll it over NVLink
+            // (cudaMemset on device memory may return before it completes; a freshly malloc'd arena can hold a
+            // previous process's epochs)
+            cuda_ok(cudaDeviceSynchronize(), "memset arena sync");
             c->peer.assign(static_cast<std::size_t>(cfg->world), nullptr);
             c->imported.assign(static_cast<std::size_t>(cfg->world), false);
             c->peer[static_cast<std::size_t>(cfg->rank)] = c->arena;
