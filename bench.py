@@ -64,12 +64,16 @@ def parse():
     ap.add_argument("--cache-params", action="store_true",
                     help="SURVEY 8(f)1: keep fetched units for the whole minibatch (one fetch per unit per step)")
     ap.add_argument("--model", default="qwen2.5-1.5b")
-    ap.add_argument("--push-mode", default="red", choices=["red", "slot"])
+    ap.add_argument("--push-mode", default="red", choices=["red", "slot", "fixed"])
     ap.add_argument("--minibs", type=int, default=8)
     ap.add_argument("--fetch-ctas", type=int, default=0)
     ap.add_argument("--push-ctas", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cap", type=int, default=32768,
+                    help="longest sample (lognormal lengths capped here) = microbatch token budget (packing ratio 1)")
+    ap.add_argument("--recompute", default="auto", choices=["auto", "none", "selective", "full"],
+                    help="activation recompute in the worker backward; auto = least recompute that fits HBM")
     return ap.parse_args()
 
 
@@ -82,11 +86,37 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def workload_lengths():
+def workload_lengths(cap=32768):
     from paper_2601_19362_b200 import partition as P
 
-    raw = P.generate_synthetic(("lognormal", 8.0, 1.5), 2048, 32768, 0)
+    raw = P.generate_synthetic(("lognormal", 8.0, 1.5), 2048, cap, 0)
     return [max(512, x) for x in raw]
+
+
+def log(*a):
+    """Progress on stderr (ODC_BENCH_LOG=1), never on the JSON stdout line."""
+    if os.environ.get("ODC_BENCH_LOG"):
+        print(f"[bench {time.strftime('%H:%M:%S')} rank {os.environ.get('RANK', '0')}]", *a, file=sys.stderr, flush=True)
+
+
+def act_bytes_per_token_layer(shape, mode):
+    """Bytes of saved activations per token per layer (worker._keep)."""
+    d, H, KV, hd, ffn = shape.d, shape.heads, shape.kv_heads, shape.head_dim, shape.ffn
+    if mode == "none":  # x a q o hm bn (bf16 d) + k v + gu m + r1 r2 lse
+        return 12 * d + 4 * KV * hd + 6 * ffn + 8 + 4 * H
+    if mode == "selective":  # x, o, lse
+        return 4 * d + 4 * H
+    return 2 * d  # x
+
+
+def pick_recompute(shape, budget_tokens, free_bytes):
+    """Least recompute whose saved activations for the largest microbatch fit
+    next to one layer's transient working set (~3x a stored layer) + 6 GB."""
+    transient = 3 * act_bytes_per_token_layer(shape, "none") * budget_tokens + (6 << 30)
+    for mode in ("none", "selective", "full"):
+        if act_bytes_per_token_layer(shape, mode) * budget_tokens * shape.layers + transient <= free_bytes:
+            return mode
+    return "full"
 
 
 def rank_plan(world, minibs, shape):
@@ -187,13 +217,14 @@ def run_reference(args):
         from paper_2601_19362_b200 import partition as P
         from paper_2601_19362_b200 import worker as W
 
-        lens = workload_lengths()
-        plan = P.plan_flat("lb-mini", lens, world, args.minibs, 32768, P.CostModel(1.0, shape.beta_over_alpha(), 1))
+        lens = workload_lengths(args.cap)
+        plan = P.plan_flat("lb-mini", lens, world, args.minibs, args.cap, P.CostModel(1.0, shape.beta_over_alpha(), 1))
         sizes = W.unit_sizes(shape)
         for k in range(args.warmup):
-            cpu_tokens_baseline(lens, plan, [k], sizes, world)
+            cpu_tokens_baseline(lens, plan, [k], sizes, world, args.minibs, args.cap, shape.beta_over_alpha())
         t0 = time.perf_counter()
-        vals = [cpu_tokens_baseline(lens, plan, [args.warmup + k], sizes, world) for k in range(args.steps)]
+        vals = [cpu_tokens_baseline(lens, plan, [args.warmup + k], sizes, world, args.minibs, args.cap,
+                                    shape.beta_over_alpha()) for k in range(args.steps)]
         wall = time.perf_counter() - t0
         tps = sum(v["value"] for v in vals) / len(vals)
         line = {"metric": METRIC, "impl": "reference", "value": round(tps, 2), "unit": "tokens/s", "n_gpus": world,
@@ -265,26 +296,37 @@ def run_sft(args):
         dist.init_process_group("nccl", device_id=dev)
     shape = SHAPES[args.model]
     sizes = W.unit_sizes(shape)
-    lens = workload_lengths()
+    lens = workload_lengths(args.cap)
+    budget = args.cap
     beta = shape.beta_over_alpha_b200() if args.cost == "b200" else shape.beta_over_alpha()
     cost = P.CostModel(1.0, beta, 1)
-    plan_odc = P.plan_flat("lb-mini", lens, world, args.minibs, 32768, cost)
-    plan_fsdp = P.plan_flat("lb-micro", lens, world, args.minibs, 32768, cost)
+    plan_odc = P.plan_flat("lb-mini", lens, world, args.minibs, budget, cost)
+    plan_fsdp = P.plan_flat("lb-micro", lens, world, args.minibs, budget, cost)
     do_fsdp = world > 1 and not args.no_fsdp
+
+    def load(target):  # identical full units on every rank, each keeps its slice
+        gen = torch.Generator(device=dev).manual_seed(0)
+        for u in range(len(sizes)):
+            full = W.init_unit(shape, u, gen, dev)
+            target.set_params(u, full)
+            del full
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
 
     eng = OdcEngine(sizes, rank=rank, world=world, device=local, push_mode=args.push_mode,
                     fetch_ctas=args.fetch_ctas, push_ctas=args.push_ctas)
-    fsdp = W.FsdpComm(sizes, rank, world, dev) if do_fsdp else None
-    gen = torch.Generator(device=dev).manual_seed(0)
-    for u in range(len(sizes)):  # identical full units on every rank, each keeps its slice
-        full = W.init_unit(shape, u, gen, dev)
-        eng.set_params(u, full)
-        if fsdp:
-            fsdp.set_params(u, full)
-        del full
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    load(eng)
+    recompute = args.recompute
+    if recompute == "auto":
+        # the FSDP arm runs after the ODC engine is released; its shards + collective
+        # buffers take the same HBM as the ODC arena (+ bf16/fp32 shard copies)
+        free = torch.cuda.mem_get_info(dev)[0] - (eng.arena_bytes() // 3 if do_fsdp else 0)
+        t = torch.tensor([float(free)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        recompute = pick_recompute(shape, budget, int(t.item()))
+    log("params loaded; arena GB", eng.arena_bytes() / 1e9, "recompute", recompute)
 
     warm_steps = list(range(args.warmup))
     timed_steps = list(range(args.warmup, args.warmup + args.steps))
@@ -293,7 +335,9 @@ def run_sft(args):
         return sum(lens[i] for dv in plan[k % len(plan)] for mb in dv for i in mb)
 
     def run_arm(comm, plan, resident: bool, record=False, clocks=None):
-        worker = W.Worker(shape, comm, dev, cache_params=args.cache_params and comm.name == "odc", attn=args.attn)
+        worker = W.Worker(shape, comm, dev, cache_params=args.cache_params and comm.name == "odc", attn=args.attn,
+                          recompute=recompute)
+        chk = eng.check if comm.name == "odc" else comm.local.check
         stream = torch.cuda.current_stream()
 
         def one(k, batches=None):
@@ -318,8 +362,9 @@ def run_sft(args):
 
         for k in warm_steps:
             one(k)
-        torch.cuda.synchronize()
-        eng.check()
+            torch.cuda.synchronize()
+            log(comm.name, "warm step", k, "done")
+        chk()
         pre = {}
         if resident:
             for k in timed_steps:
@@ -344,7 +389,8 @@ def run_sft(args):
             z.record(stream)
             torch.cuda.synchronize()
         launches = _lib.kernel_launches() - n0
-        eng.check()
+        chk()
+        log(comm.name, "timed steps done", a.elapsed_time(z), "ms")
         gsum = G.recorder.summary() if record else None
         G.recorder = None
         ms = a.elapsed_time(z)
@@ -360,11 +406,20 @@ def run_sft(args):
     clk = ClockSampler(local)
     res = run_arm(W.OdcComm(eng), plan_odc, resident=True, record=True, clocks=clk)
     e2e = run_arm(W.OdcComm(eng), plan_odc, resident=False) if not args.no_e2e else None
-    fs = run_arm(fsdp, plan_fsdp, resident=True) if do_fsdp else None
-
     if args.trace:
         write_trace(args.trace, shape, W.OdcComm(eng), plan_odc, lens, timed_steps[0], rank, world, dev)
     comm = comm_rates(eng, sizes[1], rank, world, dev)
+    fs = None
+    if do_fsdp:  # release the ODC arena first (peers are idle: synchronised + barrier)
+        torch.cuda.synchronize()
+        dist.barrier()
+        eng.check()
+        eng.close()
+        torch.cuda.empty_cache()
+        fsdp = W.FsdpComm(sizes, rank, world, dev)
+        load(fsdp)
+        fs = run_arm(fsdp, plan_fsdp, resident=True)
+        fsdp.local.close()
 
     hbm, hbm_kind = peaks()
     try:
@@ -389,15 +444,16 @@ def run_sft(args):
               for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_tokens_baseline(lens, plan_odc, timed_steps, sizes, world)
+        cpu = cpu_tokens_baseline(lens, plan_odc, timed_steps, sizes, world, args.minibs, budget, beta)
     if rank == 0:
         line = {"metric": METRIC, "value": round(res["tps"], 1), "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"] / args.steps, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (random-init weights, seeded random token ids of the workload lengths)",
                 "config": {"workload": "odc_sft", "model": shape.name, "plan": "lb-mini (odc) / lb-micro (fsdp)",
-                           "minibs_per_rank": args.minibs, "budget_tokens": 32768,
-                           "lengths": "lognormal(8,1.5) n=2048 cap=32768 seed=0, floor 512",
+                           "minibs_per_rank": args.minibs, "budget_tokens": budget,
+                           "lengths": f"lognormal(8,1.5) n=2048 cap={args.cap} seed=0, floor 512",
+                           "recompute": recompute,
                            "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
                            "cost_beta_over_alpha": round(beta, 1), "cost_model": args.cost,
                            "cache_params": args.cache_params, "attention": args.attn,
@@ -515,7 +571,7 @@ class _Null:
         return False
 
 
-def cpu_tokens_baseline(lens, plan, steps, sizes, world):
+def cpu_tokens_baseline(lens, plan, steps, sizes, world, minibs=8, budget=32768, beta=30467.0):
     """Reference CPU path of one step, extrapolated from a bounded sample: the
     reference fabric (ShardFabric<float>) moving one FSDP layer unit for one
     microbatch (2 gathers + 1 scatter_accumulate per client + finalize), times
@@ -524,7 +580,7 @@ def cpu_tokens_baseline(lens, plan, steps, sizes, world):
 
     s, _, kind, sample = cpu_reference_sample(world, sizes[1], 1)
     micro = sum(len(dv) for k in steps for dv in plan[k % len(plan)])
-    t_plan = R.plan_seconds("lb-mini", lens, world, 8, 32768, 1.0, 30467.0, 1) if R.available() else 0.0
+    t_plan = R.plan_seconds("lb-mini", lens, world, minibs, budget, 1.0, beta, 1) if R.available() else 0.0
     t = s * len(sizes) * micro / max(1, world) + t_plan * len(steps)
     toks = sum(lens[i] for k in steps for dv in plan[k % len(plan)] for mb in dv for i in mb)
     return {"value": round(toks / t, 2), "unit": "tokens/s", "cores": 1, "kind": kind,

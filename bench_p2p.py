@@ -9,6 +9,8 @@ S = bytes of one rank's bf16 parameter shard. Per rank and op:
   push           owner shards fp32 += w * grad[N*S/2 elems] (N-1 over NVLink)
   all_gather     torch.distributed.all_gather_into_tensor, same bf16 bytes
   reduce_scatter torch.distributed.reduce_scatter_tensor, same fp32 bytes
+  push_fixed     (--variants fixed:CTAS) deterministic int64 fixed-point push;
+                 GB/s counts its int64 wire bytes ((N-1)*4S)
 GB/s = algorithmic NVLink bytes per rank ((N-1)*S for bf16 gathers,
 (N-1)*2S for fp32 reductions) / op time, op time = max over ranks of the
 CUDA-event time of R back-to-back ops divided by R (barrier + sync around).
@@ -95,6 +97,9 @@ def main():
             if kind == "push":
                 e2 = OdcEngine([M], rank=rank, world=world, device=local, push_mode="red", push_ctas=int(ctas))
                 ops[f"odc_push[c={ctas}]"] = ((lambda e=e2: e.push(0, grad, 1.0)), (world - 1) * 2 * S)
+            elif kind == "fixed":  # deterministic fixed-point push: int64 on the wire (8 B/elem)
+                e2 = OdcEngine([M], rank=rank, world=world, device=local, push_mode="fixed", push_ctas=int(ctas))
+                ops[f"odc_push_fixed[c={ctas}]"] = ((lambda e=e2: e.push(0, grad, 1e-3)), (world - 1) * 4 * S)
             else:
                 e2 = OdcEngine([M], rank=rank, world=world, device=local, fetch_ctas=int(ctas), fetch_engine=kind)
                 e2.set_params(0, torch.zeros(M, device=dev))

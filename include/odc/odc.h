@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ODC_ABI_VERSION 3
+#define ODC_ABI_VERSION 4
 
 typedef enum {
     ODC_OK = 0,
@@ -55,8 +55,16 @@ typedef enum {
     ODC_PUSH_RED = 0,
     /* deterministic: per-source slot (single writer, push order), reduced by
      * the owner at the minibatch barrier in fixed rank order 0..N-1 */
-    ODC_PUSH_SLOT = 1
+    ODC_PUSH_SLOT = 1,
+    /* deterministic in bounded memory: each pushed w*g is rounded once to an
+     * int64 fixed-point value (2^-fixed_frac_bits resolution) and added into
+     * the owner's int64 accumulator with TMA bulk .add.u64 reductions over
+     * NVLink; integer sums are bit-identical for any arrival order and any
+     * world size; 8 B per owned element. Range |sum| < 2^(63-frac_bits). */
+    ODC_PUSH_FIXED = 2
 } odc_push_mode;
+
+#define ODC_FIXED_FRAC_BITS_DEFAULT 40
 
 int odc_abi_version(void);
 const char* odc_last_error(void);
@@ -123,6 +131,7 @@ typedef struct {
     int push_ctas;              /* CTAs for push  (0 = default) */
     double timeout_s;           /* device barrier watchdog (<= 0: 60 s) */
     int fetch_engine;           /* odc_fetch_engine */
+    int fixed_frac_bits;        /* ODC_PUSH_FIXED resolution 2^-bits (0 = default 40; 8..60) */
 } odc_config;
 
 typedef enum {

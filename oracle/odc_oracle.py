@@ -754,6 +754,26 @@ def slot_mode_reduce(ranks: int, elems: int, pushes, dtype=np.float32) -> np.nda
     return acc
 
 
+def fixed_mode_reduce(elems: int, pushes, frac_bits: int = 40) -> np.ndarray:
+    """FIXED push mode (no reference counterpart: the reference's
+    determinism comes from integer payloads, inc/primitives.hpp:130-131 with
+    T = int64, tests/test_primitives.cpp:116-130). Each push adds
+    q = round_half_even(fl32(w * g) * 2^S) into an int64 accumulator; the
+    result is fl32(sum) * 2^-S. Independent of push order, client and world
+    size. pushes = list of (client, grad, weight)."""
+    acc = np.zeros(elems, np.int64)
+    scale = np.float32(2.0 ** frac_bits)
+    lim = np.float32(2.0 ** 63)
+    with np.errstate(over="ignore", invalid="ignore"):
+        for _, g, w in pushes:
+            v = (np.float32(w) * np.asarray(g, np.float32)).astype(np.float32) * scale  # exact power-of-2 scaling
+            v = np.nan_to_num(v, nan=0.0)
+            q = np.where(v >= lim, np.iinfo(np.int64).max,
+                         np.where(v < -lim, np.iinfo(np.int64).min, np.rint(np.clip(v, -lim, lim)).astype(np.int64)))
+            acc += q  # int64 wraps like the device's add.u64
+    return acc.astype(np.float32) * np.float32(2.0 ** -frac_bits)
+
+
 def adamw_reference(p, g, m, v, step, lr, beta1, beta2, eps, wd):
     """fp32 AdamW, torch.optim.AdamW(foreach=False) semantics (no reference
     counterpart in odcsim: parity unpinned by the reference)."""

@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("ODC_LIB_PATH") or os.path.join(PKG, "lib", "libodc.so
 ODC_OK, ODC_ERR_PARAM, ODC_ERR_INFEASIBLE, ODC_ERR_INVARIANT = 0, 2, 3, 4
 ODC_ERR_PROTOCOL, ODC_ERR_STATE, ODC_ERR_MODE, ODC_ERR_CUDA, ODC_ERR_TIMEOUT = 5, 6, 7, 8, 9
 ODC_I64, ODC_F64, ODC_F32, ODC_BF16 = 0, 1, 2, 3
-ODC_PUSH_RED, ODC_PUSH_SLOT = 0, 1
+ODC_PUSH_RED, ODC_PUSH_SLOT, ODC_PUSH_FIXED = 0, 1, 2
+ODC_FIXED_FRAC_BITS_DEFAULT = 40
 ODC_FETCH_TMA, ODC_FETCH_LDG, ODC_FETCH_CE = 0, 1, 2
 
 i64, i64p, vp = C.c_int64, C.POINTER(C.c_int64), C.c_void_p
@@ -24,7 +25,7 @@ i64, i64p, vp = C.c_int64, C.POINTER(C.c_int64), C.c_void_p
 class OdcConfig(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("device", C.c_int), ("n_layers", C.c_int),
                 ("layer_elems", i64p), ("push_mode", C.c_int), ("fetch_ctas", C.c_int), ("push_ctas", C.c_int),
-                ("timeout_s", C.c_double), ("fetch_engine", C.c_int)]
+                ("timeout_s", C.c_double), ("fetch_engine", C.c_int), ("fixed_frac_bits", C.c_int)]
 
 
 class OdcAdamCfg(C.Structure):
@@ -109,7 +110,7 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.odc_abi_version() != 3:
+        if L.odc_abi_version() != 4:
             raise ImportError("libodc.so ABI version mismatch")
         _lib = L
     return _lib

@@ -376,8 +376,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             mx *= sl2;  // scale > 0: max commutes with the scaling
             float m_new = m;
             if (mx > m + kRescaleThreshold || m == -INFINITY) m_new = fmaxf(mx, m);
-            if (j > 0 && m_new != m) {  // lazy rescale of O_t (PV_t of j-1 completed before S_t of j)
-                const float alpha = ex2(m - m_new);
+            // lazy rescale of O_t (PV_t of j-1 completed before S_t of j). tcgen05.ld/st are
+            // warp-collective (.sync.aligned): the decision is a warp vote, rows whose max did
+            // not move rescale by 1
+            if (__any_sync(0xffffffffu, j > 0 && m_new != m)) {
+                const float alpha = m_new != m ? ex2(m - m_new) : 1.f;
                 l0 *= alpha;
                 l1 *= alpha;
 #pragma unroll 1

@@ -11,6 +11,7 @@
 //     master f32  [block+4]                               buffers, so fetch
 //     m, v   f32  [block+4]                               and push run the
 //     slot   f32  [M_l]      (SLOT push mode only)        16-byte vector path)
+//     acc    i64  [block+2]  (FIXED push mode only) stored at pad = begin % 2
 //
 // Mapping onto the reference (inc/ = /root/reference/proj/include/odcsim/):
 //   layout          ShardState ctor/shard_begin/shard_len     inc/primitives.hpp:38-56
@@ -29,6 +30,9 @@
 //   * minibatch_end: st.release.sys done[rank] into every owner, then waits
 //     ld.acquire.sys done[c] >= epoch for every client c;
 //   * AdamW then st.release.sys param_epoch = ++adams.
+//   * FIXED push into owner r waits acc_epoch[r] >= minibatches completed
+//     here: the owner converts its int64 sums to the fp32 grad shard and
+//     zeroes them right after the barrier, then publishes acc_epoch.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -60,13 +64,14 @@ constexpr std::int64_t kFlagsBytes = 4096;
 constexpr std::int64_t kDoneOff = 0;
 constexpr std::int64_t kEpochOff = 1024;
 constexpr std::int64_t kErrOff = 2048;
+constexpr std::int64_t kAccEpochOff = 3072;  // FIXED mode: minibatch whose accumulator the owner has drained
 constexpr std::uint64_t kBlobMagic = 0x4f44433142323030ULL;  // "ODC1B200"
 
 std::int64_t round256(std::int64_t x) { return (x + 255) / 256 * 256; }
 
 struct Unit {
     std::int64_t elems = 0, block = 0;
-    std::int64_t off_param = 0, off_grad = 0, off_master = 0, off_m = 0, off_v = 0, off_slot = -1;
+    std::int64_t off_param = 0, off_grad = 0, off_master = 0, off_m = 0, off_v = 0, off_slot = -1, off_acc = -1;
     std::int64_t begin(int r) const { return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r) * block); }
     std::int64_t len(int r) const { return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r + 1) * block) - begin(r); }
 };
@@ -101,10 +106,13 @@ struct odc_ctx {
     int world() const { return cfg.world; }
     int rank() const { return cfg.rank; }
     bool slot_mode() const { return cfg.push_mode == ODC_PUSH_SLOT; }
+    bool fixed_mode() const { return cfg.push_mode == ODC_PUSH_FIXED; }
+    float fixed_scale() const { return std::ldexp(1.0f, cfg.fixed_frac_bits); }
 
     char* at(int r, std::int64_t off) const { return peer[static_cast<std::size_t>(r)] + off; }
     unsigned long long* done_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kDoneOff)); }
     unsigned long long* epoch_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kEpochOff)); }
+    unsigned long long* acc_epoch_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kAccEpochOff)); }
     unsigned long long* err() const { return reinterpret_cast<unsigned long long*>(arena + kErrOff); }
     // element 0 of owner r's shard of unit u in each array
     unsigned short* param_of(int r, const Unit& u) const {
@@ -112,6 +120,10 @@ struct odc_ctx {
     }
     float* f32_of(int r, std::int64_t off, const Unit& u) const {
         return reinterpret_cast<float*>(at(r, off)) + u.begin(r) % 4;
+    }
+    // FIXED mode int64 accumulator: element parity == global index parity
+    long long* acc_of(int r, const Unit& u) const {
+        return reinterpret_cast<long long*>(at(r, u.off_acc)) + u.begin(r) % 2;
     }
     const Unit& unit(int l) const {
         if (l < 0 || l >= static_cast<int>(units.size())) throw ParamError("layer index out of range");
@@ -184,18 +196,23 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
         if (cfg->world < 1 || cfg->world > odc::kMaxSeg) throw ParamError("world must be 1..16");
         if (cfg->rank < 0 || cfg->rank >= cfg->world) throw ParamError("rank out of range");
         if (cfg->n_layers < 1 || !cfg->layer_elems) throw ParamError("need at least one FSDP unit");
-        if (cfg->push_mode != ODC_PUSH_RED && cfg->push_mode != ODC_PUSH_SLOT) throw ParamError("bad push mode");
+        if (cfg->push_mode != ODC_PUSH_RED && cfg->push_mode != ODC_PUSH_SLOT && cfg->push_mode != ODC_PUSH_FIXED)
+            throw ParamError("bad push mode");
+        if (cfg->fixed_frac_bits != 0 && (cfg->fixed_frac_bits < 8 || cfg->fixed_frac_bits > 60))
+            throw ParamError("fixed_frac_bits must be 0 (default) or 8..60");
         if (cfg->fetch_engine < ODC_FETCH_TMA || cfg->fetch_engine > ODC_FETCH_CE) throw ParamError("bad fetch engine");
         auto* c = new odc_ctx();
         try {
             c->cfg = *cfg;
             c->cfg.layer_elems = nullptr;
+            if (c->cfg.fixed_frac_bits == 0) c->cfg.fixed_frac_bits = ODC_FIXED_FRAC_BITS_DEFAULT;
             if (cfg->timeout_s > 0) c->timeout_ns = static_cast<long long>(cfg->timeout_s * 1e9);
             std::int64_t off = kFlagsBytes;
             std::uint64_t h = 1469598103934665603ULL;
             auto mix = [&](std::uint64_t v) { h = (h ^ v) * 1099511628211ULL; };
             mix(static_cast<std::uint64_t>(cfg->world));
             mix(static_cast<std::uint64_t>(cfg->push_mode));
+            mix(static_cast<std::uint64_t>(c->cfg.fixed_frac_bits));
             for (int l = 0; l < cfg->n_layers; ++l) {
                 Unit u;
                 u.elems = cfg->layer_elems[l];
@@ -216,6 +233,10 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
                 if (cfg->push_mode == ODC_PUSH_SLOT) {
                     u.off_slot = off;
                     off += round256(u.elems * 4);
+                }
+                if (cfg->push_mode == ODC_PUSH_FIXED) {
+                    u.off_acc = off;
+                    off += round256((u.block + 2) * 8);
                 }
                 c->units.push_back(u);
             }
@@ -404,6 +425,22 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
             c->pushed[static_cast<std::size_t>(layer)] = 1;
             return;
         }
+        if (c->fixed_mode()) {
+            odc::FixTable t{};
+            t.n = c->world();
+            for (int i = 0; i < c->world(); ++i) {
+                const int r = c->owner_at(i);
+                t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
+                t.dst[i] = c->acc_of(r, u);
+                t.elems[i] = u.len(r);
+                t.gate[i] = c->acc_epoch_of(r);
+            }
+            t.need = c->mb_epoch;  // the owner drained (converted + zeroed) the previous minibatch's sums
+            t.err = c->err();
+            t.timeout_ns = c->timeout_ns;
+            cuda_ok(odc::launch_push_fixed(t, weight, c->fixed_scale(), bf16, c->cfg.push_ctas, S(stream)), "push (fixed)");
+            return;
+        }
         odc::RedTable t{};
         t.n = c->world();
         for (int i = 0; i < c->world(); ++i) {
@@ -448,6 +485,19 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
             }
             cuda_ok(odc::launch_accumulate<float>(slot + u.begin(target) + offset, payload, n, weight, S(stream)),
                     "slot slice");
+            return;
+        }
+        if (c->fixed_mode()) {
+            odc::FixTable t{};
+            t.n = 1;
+            t.src[0] = payload;
+            t.dst[0] = c->acc_of(target, u) + offset;
+            t.elems[0] = n;
+            t.gate[0] = c->acc_epoch_of(target);
+            t.need = c->mb_epoch;
+            t.err = c->err();
+            t.timeout_ns = c->timeout_ns;
+            cuda_ok(odc::launch_push_fixed(t, weight, c->fixed_scale(), false, 8, S(stream)), "push_slice (fixed)");
             return;
         }
         odc::RedTable t{};
@@ -506,6 +556,23 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
                         "slot reduce");
             }
             std::fill(c->pushed.begin(), c->pushed.end(), 0);
+        }
+        if (c->fixed_mode()) {  // every client's reductions landed before its done flag: convert + zero
+            const int me = c->rank();
+            const float inv = std::ldexp(1.0f, -c->cfg.fixed_frac_bits);
+            odc::FixFinal f{};
+            for (const Unit& u : c->units) {
+                if (u.len(me) <= 0) continue;
+                f.grad[f.n] = c->f32_of(me, u.off_grad, u);
+                f.acc[f.n] = c->acc_of(me, u);
+                f.elems[f.n] = u.len(me);
+                if (++f.n == odc::kMaxFinal) {
+                    cuda_ok(odc::launch_fixed_finalize(f, inv, S(stream)), "fixed finalize");
+                    f.n = 0;
+                }
+            }
+            cuda_ok(odc::launch_fixed_finalize(f, inv, S(stream)), "fixed finalize");
+            cuda_ok(odc::launch_publish(c->acc_epoch_of(me), c->mb_epoch, S(stream)), "publish acc epoch");
         }
     });
 }

@@ -11,6 +11,10 @@
 //   slot_accumulate push (a6), SLOT mode: single-writer per-source slot
 //                   acc += w*g (local HBM), deterministic.
 //   reduce_sources  owner reduce in fixed rank order (SLOT mode barrier step)
+//   push_fixed      push (a6), FIXED mode: w*g rounded to int64 fixed point,
+//                   TMA bulk .add.u64 reductions into the owner (deterministic
+//                   in any order, 8 B per owned element); fixed_finalize
+//                   converts back to fp32 at the barrier
 //   barrier         (a8) finalize_minibatch :199-203 as sys-scope flags
 //   adam            (a19) fused AdamW over owned shards, bf16 shard out
 //   accumulate<T>   ShardState::consume :125-136 exactly (mul, then add)
@@ -583,6 +587,157 @@ cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc
     if (ctas <= 0) ctas = 296;
     count_launch();
     reduce_sources_kernel<<<ctas, 512, 0, s>>>(dst, sl, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ push (FIXED)
+// Deterministic push in bounded memory: every pushed value is
+// rounded once to a 64-bit fixed-point integer, q = rn(fl(w*g) * 2^S), and
+// added into the owner's int64 accumulator with TMA bulk reductions
+// (cp.reduce.async.bulk .add.u64, peer HBM over NVLink). Integer addition is
+// associative, so the owner's sum is bit-identical for every arrival order,
+// every interleaving of clients and every world size; the memory cost is
+// 8 B per OWNED element (SLOT mode needs 4 B per element of every unit).
+// cvt.rni.s64.f32 rounds to nearest even, clamps out-of-range values and maps
+// NaN to 0. Range: |sum| < 2^(63-S) (2^23 at the default S = 40).
+constexpr int kFixThreads = 256;
+constexpr int kFixPairs = 2;                                     // element pairs per thread per chunk
+constexpr std::int64_t kFixChunk = kFixThreads * kFixPairs;      // pairs per chunk (1024 elements, 8 KB)
+constexpr int kFixStages = 4;
+
+__device__ __forceinline__ long long to_fixed(float w, float g, float scale) {
+    return __float2ll_rn(__fmul_rn(__fmul_rn(w, g), scale));
+}
+__device__ __forceinline__ void red_sys_u64(long long* p, long long v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <bool BF16>
+__device__ __forceinline__ float2 load_grad2(const void* src, std::int64_t e) {
+    if constexpr (BF16) {
+        const unsigned v = *reinterpret_cast<const unsigned*>(reinterpret_cast<const unsigned short*>(src) + e);
+        return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+    } else {
+        return *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(src) + e);
+    }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kFixThreads) push_fixed_kernel(FixTable t, float w, float scale) {
+    __shared__ __align__(128) long long stage[kFixStages][2 * kFixChunk];
+    __shared__ std::int64_t head[kMaxSeg], lo[kMaxSeg], hi[kMaxSeg];
+    __shared__ bool fast[kMaxSeg];
+    __shared__ int gate_ok;
+    if (threadIdx.x == 0) gate_ok = 1;
+    __syncthreads();
+    // the owner converted and zeroed its accumulator at its last minibatch end
+    if (threadIdx.x < t.n && t.gate[threadIdx.x] && !wait_geq(t.gate[threadIdx.x], t.need, t.err, t.timeout_ns))
+        gate_ok = 0;
+    if (threadIdx.x < t.n) {
+        const int i = threadIdx.x;
+        // dst element index parity == global element parity (pad = begin % 2),
+        // so after at most one head element the body is 16 B aligned in dst and
+        // 8 B (4 B for bf16) aligned in src
+        const std::int64_t n = t.elems[i];
+        const std::int64_t h = (reinterpret_cast<uintptr_t>(t.dst[i]) & 15) ? 1 : 0;
+        const uintptr_t s_body = reinterpret_cast<uintptr_t>(t.src[i]) + h * (BF16 ? 2 : 4);
+        fast[i] = (reinterpret_cast<uintptr_t>(t.dst[i]) & 7) == 0 && s_body % (BF16 ? 4 : 8) == 0;
+        head[i] = n > 0 ? h : 0;
+        const std::int64_t pairs = (fast[i] && n > h) ? (n - h) / 2 : 0;
+        lo[i] = pairs * blockIdx.x / gridDim.x;
+        hi[i] = pairs * (blockIdx.x + 1) / gridDim.x;
+    }
+    __syncthreads();
+    if (!gate_ok) return;
+    // the gates were acquired through the generic proxy; the reductions go through the async proxy
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    std::int64_t maxlen = 0;
+    for (int i = 0; i < t.n; ++i) maxlen = i64max(maxlen, hi[i] - lo[i]);
+    int it = 0;
+    for (std::int64_t k = 0; k < maxlen; k += kFixChunk) {
+        for (int i = 0; i < t.n; ++i) {
+            const std::int64_t beg = lo[i] + k;
+            const std::int64_t end = i64min(hi[i], beg + kFixChunk);
+            if (beg >= end) continue;
+            long long* buf = stage[it % kFixStages];
+            if (it >= kFixStages) {  // the bulk reduction that last read this stage has finished reading it
+                if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kFixStages - 1) : "memory");
+                __syncthreads();
+            }
+            const std::int64_t e0 = head[i] + 2 * beg;  // element offset of the chunk in the segment
+            const std::int64_t np = end - beg;
+#pragma unroll
+            for (int q = 0; q < kFixPairs; ++q) {
+                const std::int64_t pi = threadIdx.x + q * kFixThreads;
+                if (pi < np) {
+                    const float2 g = load_grad2<BF16>(t.src[i], e0 + 2 * pi);
+                    const long long a = to_fixed(w, g.x, scale), b = to_fixed(w, g.y, scale);
+                    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(static_cast<unsigned>(
+                                     __cvta_generic_to_shared(buf + 2 * pi))),
+                                 "l"(a), "l"(b)
+                                 : "memory");
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
+                                 t.dst[i] + e0),
+                             "r"(static_cast<unsigned>(__cvta_generic_to_shared(buf))),
+                             "r"(static_cast<unsigned>(np * 16))
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            ++it;
+        }
+    }
+    if (threadIdx.x == 0) {  // reductions complete, then ordered before the barrier's release (later kernel)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __threadfence_system();
+    }
+    for (int i = 0; i < t.n; ++i)  // segments whose src/dst alignment rules out the bulk path: scalar reductions
+        if (!fast[i])
+            for (std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * kFixThreads + threadIdx.x; e < t.elems[i];
+                 e += static_cast<std::int64_t>(gridDim.x) * kFixThreads)
+                red_sys_u64(t.dst[i] + e, to_fixed(w, load_grad<BF16>(t.src[i], e), scale));
+    if (blockIdx.x == gridDim.x - 1) {  // ragged head / odd tail element of each bulk segment
+        for (int i = threadIdx.x; i < t.n; i += kFixThreads) {
+            const std::int64_t n = t.elems[i];
+            if (n <= 0 || !fast[i]) continue;
+            if (head[i]) red_sys_u64(t.dst[i], to_fixed(w, load_grad<BF16>(t.src[i], 0), scale));
+            const std::int64_t body_end = head[i] + 2 * ((n - head[i]) / 2);
+            if (body_end < n) red_sys_u64(t.dst[i] + body_end, to_fixed(w, load_grad<BF16>(t.src[i], body_end), scale));
+        }
+    }
+}
+
+cudaError_t launch_push_fixed(const FixTable& t, float w, float scale, bool src_bf16, int ctas, cudaStream_t s) {
+    if (t.n <= 0) return cudaSuccess;
+    if (ctas <= 0) ctas = 148;
+    count_launch();
+    if (src_bf16) push_fixed_kernel<true><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+    else push_fixed_kernel<false><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+    return cudaGetLastError();
+}
+
+// owner side, after the minibatch barrier: grad = fl(acc) * 2^-S, acc = 0
+__global__ void __launch_bounds__(512) fixed_finalize_kernel(FixFinal f, float inv_scale) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (int s = 0; s < f.n; ++s) {
+        float* g = f.grad[s];
+        long long* a = f.acc[s];
+        for (std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < f.elems[s];
+             e += stride) {
+            g[e] = __fmul_rn(__ll2float_rn(a[e]), inv_scale);
+            a[e] = 0;
+        }
+    }
+}
+
+cudaError_t launch_fixed_finalize(const FixFinal& f, float inv_scale, cudaStream_t s) {
+    if (f.n <= 0) return cudaSuccess;
+    count_launch();
+    fixed_finalize_kernel<<<148 * 4, 512, 0, s>>>(f, inv_scale);
     return cudaGetLastError();
 }
 

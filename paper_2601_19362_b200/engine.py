@@ -26,7 +26,7 @@ import torch
 from . import _lib
 from ._lib import check, lib
 
-PUSH_MODES = {"red": _lib.ODC_PUSH_RED, "slot": _lib.ODC_PUSH_SLOT}
+PUSH_MODES = {"red": _lib.ODC_PUSH_RED, "slot": _lib.ODC_PUSH_SLOT, "fixed": _lib.ODC_PUSH_FIXED}
 FETCH_ENGINES = {"tma": _lib.ODC_FETCH_TMA, "ldg": _lib.ODC_FETCH_LDG, "ce": _lib.ODC_FETCH_CE}
 
 
@@ -46,7 +46,7 @@ def _ptr(t: torch.Tensor):
 class OdcEngine:
     def __init__(self, layer_elems: Sequence[int], rank: int = 0, world: int = 1, device: Optional[int] = None,
                  push_mode: str = "red", fetch_ctas: int = 0, push_ctas: int = 0, timeout_s: float = 60.0,
-                 group=None, fetch_engine: str = "tma"):
+                 group=None, fetch_engine: str = "tma", fixed_frac_bits: int = 0):
         self.layer_elems = [int(x) for x in layer_elems]
         self.rank, self.world = rank, world
         if device is None:
@@ -55,7 +55,8 @@ class OdcEngine:
         self.push_mode = push_mode
         arr = (C.c_int64 * len(self.layer_elems))(*self.layer_elems)
         cfg = _lib.OdcConfig(rank, world, self.device, len(self.layer_elems), arr, PUSH_MODES[push_mode], fetch_ctas,
-                             push_ctas, timeout_s, FETCH_ENGINES[fetch_engine])
+                             push_ctas, timeout_s, FETCH_ENGINES[fetch_engine], fixed_frac_bits)
+        self.fixed_frac_bits = fixed_frac_bits or _lib.ODC_FIXED_FRAC_BITS_DEFAULT
         h = C.c_void_p()
         check(lib().odc_ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h

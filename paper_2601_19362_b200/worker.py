@@ -13,8 +13,11 @@ Dense layers are tcgen05 GEMMs (csrc/gemm.cu, operands used in place);
 attention is flash-attn varlen (library, sm_100 build); the elementwise
 glue (RMSNorm, bias+RoPE+split, SwiGLU, CE) is fused sm_100a kernels
 (csrc/worker_kernels.cu) and residual adds ride in the GEMM epilogue.
-Activations are kept for the backward (no recompute; they fit 180 GB for the
-1.5B shape at 32K tokens).
+Activations are kept for the backward by default (they fit 180 GB for the
+1.5B shape at 32K tokens). The 8B/14B shapes at 32K/64K tokens do not fit, so
+`recompute` keeps only each layer's input (+ the attention output and lse in
+"selective" mode) and re-runs the layer's forward in the backward, right
+after the backward's own re-fetch of the unit (no extra communication).
 
 Comm backends share one interface:
   OdcComm   odc fetch / push / device barrier / fused AdamW (libodc.so)
@@ -272,10 +275,13 @@ def attach_attn_items(b: Batch, seq_lens: Sequence[int], heads: int, device, kv_
 
 class Worker:
     def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192, max_positions: int = 65536,
-                 cache_params: bool = False, attn: str = "tcgen05"):
+                 cache_params: bool = False, attn: str = "tcgen05", recompute: str = "none"):
         if _flash_attn_varlen_forward is None:
             raise ImportError("flash-attn (sm_100) is required for the worker's attention")
         self.s, self.comm, self.dev = shape, comm, torch.device(device)
+        if recompute not in ("none", "selective", "full"):
+            raise ValueError(f"recompute must be none|selective|full, got {recompute!r}")
+        self.recompute = recompute
         self.sizes = unit_sizes(shape)
         self.L = shape.layers
         self.ce_chunk = ce_chunk
@@ -323,6 +329,48 @@ class Worker:
         ev.record(self.comm_stream)
         return ev
 
+    # --- one decoder layer forward (also the recompute of the backward)
+    def _layer_fwd(self, P, x, b: Batch, o_lse=None, out: bool = True):
+        """Returns the activations the backward needs and the layer output.
+        With `o_lse` (selective recompute) the attention forward is skipped;
+        without `out` (any recompute) so is the down projection."""
+        s = self.s
+        hd, H, KV = s.head_dim, s.heads, s.kv_heads
+        T = b.tokens
+        a, r1 = F.rmsnorm_fwd(x, P["ln1"])
+        qkv = G.linear_fwd(a, P["qkv_w"])
+        q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), self.rope, b.positions, H, KV, hd)
+        del qkv
+        if o_lse is not None:
+            o, lse = o_lse
+        elif self.attn == "tcgen05":
+            o, lse = F.attn_fwd(q, k, v, b.attn_items, 1.0 / math.sqrt(hd))
+        else:
+            o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len,
+                                                      0.0, 1.0 / math.sqrt(hd), True)
+        hm = G.linear_fwd(o.view(T, H * hd), P["o_w"], residual=x)
+        bn, r2 = F.rmsnorm_fwd(hm, P["ln2"])
+        gu = G.linear_fwd(bn, P["gu_w"])
+        m = F.swiglu_fwd(gu, s.ffn)
+        h = G.linear_fwd(m, P["down_w"], residual=hm) if out else None
+        return (x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m), h
+
+    def _keep(self, act):
+        """What the forward keeps per layer: everything (none), the layer input
+        plus the attention output and lse (selective: the backward recomputes
+        the GEMMs and glue but not the attention), or the layer input (full)."""
+        if self.recompute == "none":
+            return act
+        if self.recompute == "selective":
+            return (act[0], act[6], act[7])
+        return (act[0],)
+
+    def _restore(self, P, kept, b: Batch):
+        if self.recompute == "none":
+            return kept
+        o_lse = (kept[1], kept[2]) if self.recompute == "selective" else None
+        return self._layer_fwd(P, kept[0], b, o_lse, out=False)[0]
+
     def microbatch(self, b: Batch, weight: float) -> torch.Tensor:
         s, L = self.s, self.L
         cur = torch.cuda.current_stream(self.dev)
@@ -347,23 +395,9 @@ class Worker:
             P = views(self._ubuf(l), lay)
             if l < L:  # prefetch the next unit into the other buffer once layer l-1 released it
                 ev = self._fetch_unit(l + 1, after=_record(cur))
-            x = h
             tr = self.tracer.span("fwd", l, cur, False) if self.tracer else None
-            a, r1 = F.rmsnorm_fwd(x, P["ln1"])
-            qkv = G.linear_fwd(a, P["qkv_w"])
-            q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), tab, b.positions, H, KV, hd)
-            del qkv
-            if self.attn == "tcgen05":
-                o, lse = F.attn_fwd(q, k, v, b.attn_items, scale)
-            else:
-                o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len,
-                                                          0.0, scale, True)
-            hm = G.linear_fwd(o.view(T, H * hd), P["o_w"], residual=x)
-            bn, r2 = F.rmsnorm_fwd(hm, P["ln2"])
-            gu = G.linear_fwd(bn, P["gu_w"])
-            m = F.swiglu_fwd(gu, s.ffn)
-            h = G.linear_fwd(m, P["down_w"], residual=hm)
-            saved.append((x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m))
+            act, h = self._layer_fwd(P, h, b)
+            saved.append(self._keep(act))
             if tr:
                 Tracer.end(tr, cur)
 
@@ -406,8 +440,8 @@ class Worker:
             for name in ("ln1", "ln2", "qkv_b"):  # atomically accumulated parts
                 if name in Gv:
                     Gv[name].zero_()
-            x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = saved[l - 1]
             tr = self.tracer.span("bwd", l, cur, False) if self.tracer else None
+            x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = self._restore(P, saved[l - 1], b)
             # MLP block
             dm = G.linear_dgrad(dh, P["down_w"])
             G.linear_wgrad(dh, m, out=Gv["down_w"])

@@ -23,7 +23,7 @@ def _bf16_bits(x: torch.Tensor):
     return x.view(torch.int16).cpu().numpy()
 
 
-@pytest.mark.parametrize("mode", ["red", "slot"])
+@pytest.mark.parametrize("mode", ["red", "slot", "fixed"])
 def test_set_params_fetch_roundtrip(mode):
     eng = OdcEngine(SIZES, push_mode=mode)
     g = torch.Generator(device="cpu").manual_seed(0)
@@ -78,7 +78,7 @@ def test_push_slice_protocol_errors_and_values():
     assert eng.read_grad_shard(0).cpu().tolist() == [0, 0, 1, 1, 1, 0, 0, 0, 0, 0]
 
 
-@pytest.mark.parametrize("mode", ["red", "slot"])
+@pytest.mark.parametrize("mode", ["red", "slot", "fixed"])
 def test_adam_matches_torch_adamw(mode):
     sizes = [1001, 65536 + 3, 8]
     eng = OdcEngine(sizes, push_mode=mode)
@@ -93,6 +93,8 @@ def test_adam_matches_torch_adamw(mode):
         for l, g in enumerate(grads):
             eng.push(l, g, 1.0)
             ref[l].grad = g.clone()
+            if mode == "fixed":  # the optimizer sees the fixed-point-rounded gradient
+                ref[l].grad = torch.from_numpy(O.fixed_mode_reduce(g.numel(), [(0, g.cpu().numpy(), 1.0)])).to(DEV)
         eng.minibatch_end()
         eng.adam_step(lr=1e-2, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
         opt.step()
@@ -105,6 +107,55 @@ def test_adam_matches_torch_adamw(mode):
             torch.cuda.synchronize()
             assert torch.equal(out, got.to(torch.bfloat16))
             assert not eng.read_grad_shard(l).any()  # grads zeroed for the next minibatch
+
+
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])
+def test_fixed_push_is_order_independent_and_matches_oracle(gdt):
+    """FIXED mode: the owner's sum is the same bits whatever the
+    push order, and equals the oracle's int64 fixed-point sum exactly."""
+    rng = np.random.default_rng(11)
+    pushes = {l: [] for l in range(len(SIZES))}
+    for k in range(4):
+        for l, n in enumerate(SIZES):
+            g = (rng.standard_normal(n) * 10.0 ** rng.integers(-6, 3, n)).astype(np.float32)
+            g = torch.from_numpy(g).to(gdt).float().numpy()  # what a bf16 push carries
+            pushes[l].append((0, g, np.float32(rng.random())))
+    results = []
+    for order in (lambda p: p, lambda p: p[::-1], lambda p: [p[2], p[0], p[3], p[1]]):
+        eng = OdcEngine(SIZES, push_mode="fixed")
+        for l, n in enumerate(SIZES):
+            eng.set_params(l, torch.zeros(n, device=DEV))
+        for l in range(len(SIZES)):
+            for _, g, w in order(pushes[l]):
+                eng.push(l, torch.from_numpy(g).to(DEV).to(gdt), float(w))
+        eng.minibatch_end()
+        eng.check()
+        results.append([eng.read_grad_shard(l).cpu().numpy() for l in range(len(SIZES))])
+        eng.close()
+    for l, n in enumerate(SIZES):
+        want = O.fixed_mode_reduce(n, pushes[l])
+        for r in results:
+            assert np.array_equal(r[l].view(np.int32), want.view(np.int32)), l
+        # and it is a faithful fp32 sum: rel 1e-5 of the float64 sum (norm-wise)
+        exact = sum(np.float64(w) * g.astype(np.float64) for _, g, w in pushes[l])
+        assert np.linalg.norm(want - exact) <= 1e-5 * np.linalg.norm(exact) + 1e-9
+
+
+def test_fixed_push_slice_and_second_minibatch():
+    eng = OdcEngine([10, 7], push_mode="fixed")
+    with pytest.raises(E.ProtocolError):
+        eng.push_slice(0, 0, 5, torch.ones(6, device=DEV), 1.0)
+    eng.push_slice(0, 0, 3, torch.full((3,), 2.0, device=DEV), 0.5)  # odd offset: unaligned path
+    eng.push(1, torch.arange(7, dtype=torch.float32, device=DEV), 0.25)
+    eng.minibatch_end()
+    assert eng.read_grad_shard(0).cpu().tolist() == [0, 0, 0, 1, 1, 1, 0, 0, 0, 0]
+    assert eng.read_grad_shard(1).cpu().tolist() == [0, 0.25, 0.5, 0.75, 1.0, 1.25, 1.5]
+    # no AdamW in between: the accumulators were drained at the barrier
+    eng.push(1, torch.ones(7, device=DEV), 1.0)
+    eng.minibatch_end()
+    eng.check()
+    assert eng.read_grad_shard(1).cpu().tolist() == [1.0] * 7
+    assert eng.read_grad_shard(0).cpu().tolist() == [0.0] * 10
 
 
 def test_full_size_unit_roundtrip_and_accumulate():

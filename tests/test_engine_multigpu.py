@@ -74,10 +74,11 @@ def _worker(rank, world, port, mode, q):
             eng.check()
             for l, n in enumerate(SIZES):
                 pushes = [(c, *_grads(epoch, c, k, n, l)) for c in range(world) for k in range(counts[c])]
-                want_full = O.slot_mode_reduce(world, n, pushes, np.float32)
+                want_full = (O.fixed_mode_reduce(n, pushes) if mode == "fixed"
+                             else O.slot_mode_reduce(world, n, pushes, np.float32))
                 b, ln = eng.shard_range(l)
                 got = eng.read_grad_shard(l).cpu().numpy()
-                if mode == "slot":
+                if mode in ("slot", "fixed"):
                     assert np.array_equal(got, want_full[b:b + ln]), f"slot grads e={epoch} l={l}"
                 else:
                     assert np.allclose(got, want_full[b:b + ln], rtol=1e-5, atol=1e-6), f"red grads e={epoch} l={l}"
@@ -99,7 +100,7 @@ def _worker(rank, world, port, mode, q):
 
 
 @pytest.mark.skipif(not have_gpus(2), reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("mode", ["red", "slot"])
+@pytest.mark.parametrize("mode", ["red", "slot", "fixed"])
 def test_engine_multi_gpu(mode):
     import torch
     import torch.multiprocessing as mp

@@ -18,6 +18,8 @@ from paper_2601_19362_b200.shapes import Shape
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 TINY = Shape("tiny", 256, 512, 2, 2, 1, 1024, True, True)
+# Llama-3 style: no qkv bias, untied LM head, GQA group of 4, head_dim 128 (tcgen05 attention)
+TINY_LLAMA = Shape("tiny-llama", 512, 1024, 2, 4, 1, 1024, False, False)
 
 
 def ref_loss(shape, units, batch):
@@ -41,7 +43,9 @@ def ref_loss(shape, units, batch):
     for l in range(1, s.layers + 1):
         P = W.views(units[l], W.layer_layout(s))
         a = rms(h, P["ln1"])
-        qkv = a @ P["qkv_w"].t() + P["qkv_b"]
+        qkv = a @ P["qkv_w"].t()
+        if s.qkv_bias:
+            qkv = qkv + P["qkv_b"]
         hd, H, KV = s.head_dim, s.heads, s.kv_heads
         q = rope(qkv[:, :H * hd].view(T, H, hd))
         k = rope(qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd))
@@ -58,13 +62,14 @@ def ref_loss(shape, units, batch):
         gu = bn @ P["gu_w"].t()
         h = h + (F.silu(gu[:, :s.ffn]) * gu[:, s.ffn:]) @ P["down_w"].t()
     hf = rms(h, E["norm"])
-    logits = hf @ E["emb"].t()
+    logits = hf @ (E["emb"] if s.tied else E["head"]).t()
     return F.cross_entropy(logits, batch.labels, ignore_index=-100)
 
 
-def test_worker_matches_fp32_reference():
+@pytest.mark.parametrize("s,recompute", [(TINY, "none"), (TINY, "selective"), (TINY, "full"),
+                                         (TINY_LLAMA, "none"), (TINY_LLAMA, "selective")])
+def test_worker_matches_fp32_reference(s, recompute):
     torch.manual_seed(0)
-    s = TINY
     sizes = W.unit_sizes(s)
     gen = torch.Generator(device=DEV).manual_seed(0)
     units32 = [W.init_unit(s, u, gen, DEV) for u in range(len(sizes))]
@@ -75,7 +80,7 @@ def test_worker_matches_fp32_reference():
         eng.set_params(u, t)
     lens = [37, 100, 63, 200]
     batch = W.make_batch(lens, [0, 2, 3], s.vocab, DEV)
-    worker = W.Worker(s, W.OdcComm(eng), DEV, ce_chunk=128)
+    worker = W.Worker(s, W.OdcComm(eng), DEV, ce_chunk=128, recompute=recompute)
     loss = worker.microbatch(batch, 1.0)
     eng.minibatch_end()
     eng.check()
@@ -115,3 +120,28 @@ def test_param_cache_matches_refetch():
     # runs agree to fp32 rounding, not bitwise
     for a, b in zip(*grads):
         torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-7)
+
+
+def test_recompute_matches_stored_activations():
+    """Activation recompute re-runs the same kernels on the same fetched unit,
+    so the gradients must match the stored-activation path to fp32 rounding of
+    the atomically reduced parts."""
+    s = TINY_LLAMA
+    sizes = W.unit_sizes(s)
+    gen = torch.Generator(device=DEV).manual_seed(3)
+    units = [W.init_unit(s, u, gen, DEV) for u in range(len(sizes))]
+    lens = [300, 129, 64, 511]
+    grads, losses = [], []
+    for rc in ("none", "selective", "full"):
+        eng = OdcEngine(sizes, push_mode="slot")
+        for u, t in enumerate(units):
+            eng.set_params(u, t)
+        wk = W.Worker(s, W.OdcComm(eng), DEV, ce_chunk=256, recompute=rc)
+        losses.append(wk.microbatch(W.make_batch(lens, [0, 1, 2, 3], s.vocab, DEV), 1.0).item())
+        eng.minibatch_end()
+        eng.check()
+        grads.append([eng.read_grad_shard(u).clone() for u in range(len(sizes))])
+    assert max(losses) - min(losses) <= 1e-5 * abs(losses[0]), losses  # CE sums its chunks with atomics
+    for g in grads[1:]:
+        for a, b in zip(grads[0], g):
+            torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-7)
