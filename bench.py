@@ -322,6 +322,7 @@ def run_sft(args):
         # the FSDP arm runs after the ODC engine is released; its shards + collective
         # buffers take the same HBM as the ODC arena (+ bf16/fp32 shard copies)
         free = torch.cuda.mem_get_info(dev)[0] - (eng.arena_bytes() // 3 if do_fsdp else 0)
+        free -= 2 * sizes[1] * 6 + sizes[0] * 6  # the worker's unit buffers (bf16 params + fp32 grads, x2 / embedding)
         t = torch.tensor([float(free)], device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MIN)

@@ -151,3 +151,22 @@ def test_oracle_matches_live_reference_random_plans():
         for s in ("lb-mini", "lb-micro", "local-sort"):
             st, dr = O.plan(s, lens, D, mb, budget, Q, trial)
             assert O.solutions_to_json(st, dr) == R.plan_json(s, lens, D, mb, budget, 1.0, 0.0, 1, trial)
+
+
+def test_fixed_mode_oracle_is_order_independent_and_faithful():
+    """FIXED push mode has no reference counterpart; its oracle
+    must be order-independent bit for bit and within rel 1e-5 (norm-wise) of
+    the float64 sum, like the reference's integer-payload determinism
+    (tests/test_primitives.cpp:116-130)."""
+    rng = np.random.default_rng(7)
+    n = 4099
+    pushes = [(c, (rng.standard_normal(n) * 10.0 ** rng.integers(-6, 3, n)).astype(np.float32),
+               np.float32(rng.random())) for c in range(6)]
+    a = O.fixed_mode_reduce(n, pushes)
+    for perm in ([5, 4, 3, 2, 1, 0], [2, 0, 5, 1, 4, 3]):
+        assert np.array_equal(O.fixed_mode_reduce(n, [pushes[i] for i in perm]).view(np.int32), a.view(np.int32))
+    exact = sum(np.float64(w) * g.astype(np.float64) for _, g, w in pushes)
+    assert np.linalg.norm(a - exact) <= 1e-5 * np.linalg.norm(exact)
+    # exactly representable values come back exactly
+    g = np.array([0.5, -1.25, 3.0, 0.0], np.float32)
+    assert O.fixed_mode_reduce(4, [(0, g, np.float32(1.0)), (1, g, np.float32(0.5))]).tolist() == [0.75, -1.875, 4.5, 0.0]
