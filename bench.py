@@ -514,14 +514,16 @@ def comm_rates(eng, M, rank, world, dev, reps=10):
         torch.cuda.synchronize()
         ms, _, _, _ = rank_timings(a.elapsed_time(b) / reps, 0.0, 0, device=dev)
         block = (M + world - 1) // world
+        wire = 8 if eng.push_mode == "fixed" else 4  # FIXED push moves int64 fixed-point values
         if world > 1:
-            nbytes = (world - 1) * block * (2 if name == "fetch" else 4)
+            nbytes = (world - 1) * block * (2 if name == "fetch" else wire)
         else:
-            nbytes = M * (4 if name == "fetch" else 12)
+            nbytes = M * (4 if name == "fetch" else 4 + 2 * wire)
         res[name + "_GBps"] = round(nbytes / (ms / 1e3) / 1e9, 1)
         res[name + "_us"] = round(ms * 1e3, 1)
     peak = NVLINK_NOMINAL_GBS if world > 1 else peaks()[0]
-    res.update({"bytes": "NVLink per direction" if world > 1 else "local HBM read+write", "peak_GBps": peak,
+    res.update({"bytes": ("NVLink per direction" if world > 1 else "local HBM read+write")
+                + ("; push counts int64 wire bytes (FIXED mode)" if eng.push_mode == "fixed" else ""), "peak_GBps": peak,
                 "fetch_frac": round(res["fetch_GBps"] / peak, 4), "push_frac": round(res["push_GBps"] / peak, 4),
                 "unit_elems": M, "all_ranks_concurrent": True})
     return res
