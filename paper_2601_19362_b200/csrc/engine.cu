@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -426,7 +427,7 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
             return;
         }
         if (c->fixed_mode()) {
-            odc::FixTable t{};
+            odc::BulkTable t{};
             t.n = c->world();
             for (int i = 0; i < c->world(); ++i) {
                 const int r = c->owner_at(i);
@@ -438,7 +439,34 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
             t.need = c->mb_epoch;  // the owner drained (converted + zeroed) the previous minibatch's sums
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
-            cuda_ok(odc::launch_push_fixed(t, weight, c->fixed_scale(), bf16, c->cfg.push_ctas, S(stream)), "push (fixed)");
+            cuda_ok(odc::launch_push_bulk(t, true, weight, c->fixed_scale(), bf16, c->cfg.push_ctas, S(stream)),
+                    "push (fixed)");
+            return;
+        }
+        // RED engine: TMA bulk reductions (cp.reduce.async.bulk .add.f32, 8 KB per op) beat
+        // per-thread red.global.add.v4.f32 by 7-8% over NVLink from 16 MB shards up (N=2: 552 vs
+        // 514 GB/s, N=4: 567 vs 527 at 256 MB, profiles/r01/p2p_push_engines.md); red.v4 stays
+        // for small shards (< 1 M elements per owner), where its lower launch cost wins.
+        // ODC_RED_ENGINE=red|bulk pins one engine (ablation).
+        static const int red_engine = [] {
+            const char* v = std::getenv("ODC_RED_ENGINE");
+            if (!v) return 0;
+            return std::string(v) == "bulk" ? 2 : std::string(v) == "red" ? 1 : 0;
+        }();
+        if (red_engine == 2 || (red_engine == 0 && u.block >= (1 << 20))) {
+            odc::BulkTable t{};
+            t.n = c->world();
+            for (int i = 0; i < c->world(); ++i) {
+                const int r = c->owner_at(i);
+                t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
+                t.dst[i] = c->f32_of(r, u.off_grad, u);
+                t.elems[i] = u.len(r);
+                t.gate[i] = c->epoch_of(r);
+            }
+            t.need = c->adams;
+            t.err = c->err();
+            t.timeout_ns = c->timeout_ns;
+            cuda_ok(odc::launch_push_bulk(t, false, weight, 1.f, bf16, c->cfg.push_ctas, S(stream)), "push (bulk)");
             return;
         }
         odc::RedTable t{};
@@ -488,7 +516,7 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
             return;
         }
         if (c->fixed_mode()) {
-            odc::FixTable t{};
+            odc::BulkTable t{};
             t.n = 1;
             t.src[0] = payload;
             t.dst[0] = c->acc_of(target, u) + offset;
@@ -497,7 +525,7 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
             t.need = c->mb_epoch;
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
-            cuda_ok(odc::launch_push_fixed(t, weight, c->fixed_scale(), false, 8, S(stream)), "push_slice (fixed)");
+            cuda_ok(odc::launch_push_bulk(t, true, weight, c->fixed_scale(), false, 8, S(stream)), "push_slice (fixed)");
             return;
         }
         odc::RedTable t{};

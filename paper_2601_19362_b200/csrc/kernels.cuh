@@ -36,12 +36,12 @@ struct RedTable {
     long long timeout_ns = 0;
 };
 
-// fixed-point reduction segments for the deterministic bounded-memory push:
-// dst[i] += rn(w * src[i] * 2^S) in int64
-struct FixTable {
+// bulk-reduction push segments: FIXED dst[i] += rn(w * src[i] * 2^S) in
+// int64, F32 dst[i] += w * src[i] in fp32 (TMA bulk reduce into peer memory)
+struct BulkTable {
     int n = 0;
     const void* src[kMaxSeg];  // grad slice (fp32 or bf16)
-    long long* dst[kMaxSeg];   // owner's int64 accumulator (peer memory)
+    void* dst[kMaxSeg];        // owner's int64 accumulator / fp32 grad shard (peer memory)
     std::int64_t elems[kMaxSeg];
     const unsigned long long* gate[kMaxSeg];
     unsigned long long need = 0;
@@ -72,9 +72,11 @@ cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas,
 cudaError_t launch_slot_accumulate(float* acc, const void* grad, bool src_bf16, std::int64_t n, float w, bool assign,
                                    const unsigned long long* const* gates, int ngates, unsigned long long need,
                                    unsigned long long* err, long long timeout_ns, int ctas, cudaStream_t s);
-// push, FIXED mode (deterministic, bounded memory): TMA bulk add.u64 of
-// rn(w*g*scale) into every owner's int64 accumulator
-cudaError_t launch_push_fixed(const FixTable& t, float w, float scale, bool src_bf16, int ctas, cudaStream_t s);
+// push through TMA bulk reductions (cp.reduce.async.bulk): FIXED mode
+// (deterministic, bounded memory) adds rn(w*g*scale) into every owner's int64
+// accumulator; otherwise (RED mode) w*g into the owner's fp32 grad shard
+cudaError_t launch_push_bulk(const BulkTable& t, bool fixed, float w, float scale, bool src_bf16, int ctas,
+                             cudaStream_t s);
 // owner, after the barrier: grad[i] = fl(acc[i]) * inv_scale; acc[i] = 0
 cudaError_t launch_fixed_finalize(const FixFinal& f, float inv_scale, cudaStream_t s);
 // owner reduce in fixed source order: dst[i] = sum_{c=0..nsrc-1} src[c][i]

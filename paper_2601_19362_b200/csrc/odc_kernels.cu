@@ -601,9 +601,7 @@ cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc
 // cvt.rni.s64.f32 rounds to nearest even, clamps out-of-range values and maps
 // NaN to 0. Range: |sum| < 2^(63-S) (2^23 at the default S = 40).
 constexpr int kFixThreads = 256;
-constexpr int kFixPairs = 2;                                     // element pairs per thread per chunk
-constexpr std::int64_t kFixChunk = kFixThreads * kFixPairs;      // pairs per chunk (1024 elements, 8 KB)
-constexpr int kFixStages = 4;
+
 
 __device__ __forceinline__ long long to_fixed(float w, float g, float scale) {
     return __float2ll_rn(__fmul_rn(__fmul_rn(w, g), scale));
@@ -622,30 +620,42 @@ __device__ __forceinline__ float2 load_grad2(const void* src, std::int64_t e) {
     }
 }
 
-template <bool BF16>
-__global__ void __launch_bounds__(kFixThreads) push_fixed_kernel(FixTable t, float w, float scale) {
-    __shared__ __align__(128) long long stage[kFixStages][2 * kFixChunk];
+// One kernel body for both bulk pushes: every 16 B unit of the owner's shard
+// (FIXED: 2 int64, F32: 4 fp32) is produced in registers, staged in a 3-deep
+// shared-memory ring and added into peer HBM by one elected thread with
+// cp.reduce.async.bulk (.add.u64 / .add.f32). 8 KB per bulk op, 25 KB of
+// smem per CTA so four CTAs share an SM (and one fits next to a GEMM).
+constexpr int kBulkUnits = 2;   // 16 B units per thread per chunk
+constexpr int kBulkStages = 3;
+
+template <bool BF16, bool FIXED>
+__global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, float w, float scale) {
+    constexpr int E = FIXED ? 2 : 4;                 // elements per 16 B unit of dst
+    constexpr int kDstBytes = FIXED ? 8 : 4;
+    constexpr std::int64_t kChunk = kFixThreads * kBulkUnits;  // units per chunk
+    __shared__ __align__(128) uint4 stage[kBulkStages][kChunk];
     __shared__ std::int64_t head[kMaxSeg], lo[kMaxSeg], hi[kMaxSeg];
     __shared__ bool fast[kMaxSeg];
     __shared__ int gate_ok;
     if (threadIdx.x == 0) gate_ok = 1;
     __syncthreads();
-    // the owner converted and zeroed its accumulator at its last minibatch end
+    // FIXED: the owner drained its accumulator at its last minibatch end; F32: the owner's AdamW zeroed its grad shard
     if (threadIdx.x < t.n && t.gate[threadIdx.x] && !wait_geq(t.gate[threadIdx.x], t.need, t.err, t.timeout_ns))
         gate_ok = 0;
     if (threadIdx.x < t.n) {
         const int i = threadIdx.x;
-        // dst element index parity == global element parity (pad = begin % 2),
-        // so after at most one head element the body is 16 B aligned in dst and
-        // 8 B (4 B for bf16) aligned in src
+        // the owner's shard is co-aligned with its position in the caller's full-layer
+        // buffer (arena padding), so after < E head elements dst is 16 B aligned and the
+        // grad body is aligned for E-element vector loads
         const std::int64_t n = t.elems[i];
-        const std::int64_t h = (reinterpret_cast<uintptr_t>(t.dst[i]) & 15) ? 1 : 0;
+        const uintptr_t d = reinterpret_cast<uintptr_t>(t.dst[i]);
+        const std::int64_t h = i64min(n, static_cast<std::int64_t>(((16 - (d & 15)) & 15) / kDstBytes));
         const uintptr_t s_body = reinterpret_cast<uintptr_t>(t.src[i]) + h * (BF16 ? 2 : 4);
-        fast[i] = (reinterpret_cast<uintptr_t>(t.dst[i]) & 7) == 0 && s_body % (BF16 ? 4 : 8) == 0;
-        head[i] = n > 0 ? h : 0;
-        const std::int64_t pairs = (fast[i] && n > h) ? (n - h) / 2 : 0;
-        lo[i] = pairs * blockIdx.x / gridDim.x;
-        hi[i] = pairs * (blockIdx.x + 1) / gridDim.x;
+        fast[i] = d % kDstBytes == 0 && s_body % (E * (BF16 ? 2 : 4)) == 0;
+        head[i] = fast[i] ? h : 0;
+        const std::int64_t units = fast[i] ? (n - h) / E : 0;
+        lo[i] = units * blockIdx.x / gridDim.x;
+        hi[i] = units * (blockIdx.x + 1) / gridDim.x;
     }
     __syncthreads();
     if (!gate_ok) return;
@@ -654,38 +664,50 @@ __global__ void __launch_bounds__(kFixThreads) push_fixed_kernel(FixTable t, flo
     std::int64_t maxlen = 0;
     for (int i = 0; i < t.n; ++i) maxlen = i64max(maxlen, hi[i] - lo[i]);
     int it = 0;
-    for (std::int64_t k = 0; k < maxlen; k += kFixChunk) {
+    for (std::int64_t k = 0; k < maxlen; k += kChunk) {
         for (int i = 0; i < t.n; ++i) {
             const std::int64_t beg = lo[i] + k;
-            const std::int64_t end = i64min(hi[i], beg + kFixChunk);
+            const std::int64_t end = i64min(hi[i], beg + kChunk);
             if (beg >= end) continue;
-            long long* buf = stage[it % kFixStages];
-            if (it >= kFixStages) {  // the bulk reduction that last read this stage has finished reading it
-                if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kFixStages - 1) : "memory");
+            uint4* buf = stage[it % kBulkStages];
+            if (it >= kBulkStages) {  // the bulk reduction that last read this stage has finished reading it
+                if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkStages - 1) : "memory");
                 __syncthreads();
             }
-            const std::int64_t e0 = head[i] + 2 * beg;  // element offset of the chunk in the segment
-            const std::int64_t np = end - beg;
+            const std::int64_t e0 = head[i] + E * beg;  // element offset of the chunk in the segment
+            const std::int64_t nu = end - beg;
 #pragma unroll
-            for (int q = 0; q < kFixPairs; ++q) {
-                const std::int64_t pi = threadIdx.x + q * kFixThreads;
-                if (pi < np) {
-                    const float2 g = load_grad2<BF16>(t.src[i], e0 + 2 * pi);
-                    const long long a = to_fixed(w, g.x, scale), b = to_fixed(w, g.y, scale);
-                    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(static_cast<unsigned>(
-                                     __cvta_generic_to_shared(buf + 2 * pi))),
-                                 "l"(a), "l"(b)
-                                 : "memory");
+            for (int q = 0; q < kBulkUnits; ++q) {
+                const std::int64_t u = threadIdx.x + q * kFixThreads;
+                if (u < nu) {
+                    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(buf + u));
+                    if constexpr (FIXED) {
+                        const float2 g = load_grad2<BF16>(t.src[i], e0 + E * u);
+                        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(to_fixed(w, g.x, scale)),
+                                     "l"(to_fixed(w, g.y, scale))
+                                     : "memory");
+                    } else {
+                        const float4 g = load_grad4<BF16>(t.src[i], e0 + E * u);
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sa), "f"(__fmul_rn(w, g.x)),
+                                     "f"(__fmul_rn(w, g.y)), "f"(__fmul_rn(w, g.z)), "f"(__fmul_rn(w, g.w))
+                                     : "memory");
+                    }
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
             if (threadIdx.x == 0) {
-                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
-                                 t.dst[i] + e0),
-                             "r"(static_cast<unsigned>(__cvta_generic_to_shared(buf))),
-                             "r"(static_cast<unsigned>(np * 16))
-                             : "memory");
+                char* dst = static_cast<char*>(t.dst[i]) + e0 * kDstBytes;
+                const unsigned src = static_cast<unsigned>(__cvta_generic_to_shared(buf));
+                const unsigned bytes = static_cast<unsigned>(nu * 16);
+                if constexpr (FIXED)
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(src), "r"(bytes)
+                                 : "memory");
+                else
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(src), "r"(bytes)
+                                 : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
             ++it;
@@ -695,28 +717,39 @@ __global__ void __launch_bounds__(kFixThreads) push_fixed_kernel(FixTable t, flo
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         __threadfence_system();
     }
+    auto scalar = [&](int i, std::int64_t e) {
+        const float g = load_grad<BF16>(t.src[i], e);
+        if constexpr (FIXED) red_sys_u64(static_cast<long long*>(t.dst[i]) + e, to_fixed(w, g, scale));
+        else red_sys_f32(static_cast<float*>(t.dst[i]) + e, __fmul_rn(w, g));
+    };
     for (int i = 0; i < t.n; ++i)  // segments whose src/dst alignment rules out the bulk path: scalar reductions
         if (!fast[i])
             for (std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * kFixThreads + threadIdx.x; e < t.elems[i];
                  e += static_cast<std::int64_t>(gridDim.x) * kFixThreads)
-                red_sys_u64(t.dst[i] + e, to_fixed(w, load_grad<BF16>(t.src[i], e), scale));
-    if (blockIdx.x == gridDim.x - 1) {  // ragged head / odd tail element of each bulk segment
-        for (int i = threadIdx.x; i < t.n; i += kFixThreads) {
+                scalar(i, e);
+    if (blockIdx.x == gridDim.x - 1) {  // ragged head / tail elements of each bulk segment
+        for (int i = 0; i < t.n; ++i) {
             const std::int64_t n = t.elems[i];
             if (n <= 0 || !fast[i]) continue;
-            if (head[i]) red_sys_u64(t.dst[i], to_fixed(w, load_grad<BF16>(t.src[i], 0), scale));
-            const std::int64_t body_end = head[i] + 2 * ((n - head[i]) / 2);
-            if (body_end < n) red_sys_u64(t.dst[i] + body_end, to_fixed(w, load_grad<BF16>(t.src[i], body_end), scale));
+            const std::int64_t body_end = head[i] + E * ((n - head[i]) / E);
+            if (threadIdx.x < head[i]) scalar(i, threadIdx.x);
+            if (body_end + threadIdx.x < n) scalar(i, body_end + threadIdx.x);
         }
     }
 }
 
-cudaError_t launch_push_fixed(const FixTable& t, float w, float scale, bool src_bf16, int ctas, cudaStream_t s) {
+cudaError_t launch_push_bulk(const BulkTable& t, bool fixed, float w, float scale, bool src_bf16, int ctas,
+                             cudaStream_t s) {
     if (t.n <= 0) return cudaSuccess;
-    if (ctas <= 0) ctas = 148;
+    if (ctas <= 0) ctas = 148 * 4;
     count_launch();
-    if (src_bf16) push_fixed_kernel<true><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
-    else push_fixed_kernel<false><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+    if (fixed) {
+        if (src_bf16) push_bulk_kernel<true, true><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+        else push_bulk_kernel<false, true><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+    } else {
+        if (src_bf16) push_bulk_kernel<true, false><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+        else push_bulk_kernel<false, false><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
+    }
     return cudaGetLastError();
 }
 
