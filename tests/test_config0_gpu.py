@@ -1,0 +1,165 @@
+"""BASELINE configs[0] on ONE GPU: the reference's CPU workload — a small
+transformer ODC SFT step with world_size=2 simulated ranks on the fixed
+survey lengths (d=256, 4 layers, 4 heads, ffn 1024) —
+run as two real ODC ranks (two processes, both on cuda:0, arenas exchanged
+through CUDA IPC, fetch / push / device barrier / AdamW exactly as across
+GPUs), so the world=2 protocol is exercised in the single-GPU test tier.
+
+Checks:
+  * the product's LB-Mini plan of the fixture equals the golden assignment
+    (rank 0 [[4]], rank 1 [[2],[3,6,12,14],[0,1,5,7,8,9,10,11,13,15]]);
+  * FIXED push: the owned gradient shards of the two ranks, concatenated,
+    equal the same microbatches run in another order through one world=1
+    FIXED engine (rel-L2 < 1e-2: the microbatch gradients themselves are
+    non-deterministic bf16 computations; a lost or doubled contribution of
+    either rank would show as O(0.3));
+  * the step's gradient matches a plain fp32 torch autograd reference of the
+    whole minibatch (cos > 0.995, rel-L2 < 5e-2: bf16 compute)."""
+import os
+import socket
+import traceback
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LENS = [451, 131, 1078, 28, 2048, 77, 27, 63, 76, 119, 89, 601, 435, 90, 712, 264]
+GOLDEN = [[[4]], [[2], [3, 6, 12, 14], [0, 1, 5, 7, 8, 9, 10, 11, 13, 15]]]
+
+
+def _shape():
+    from paper_2601_19362_b200.shapes import Shape
+
+    return Shape("config0", 256, 1024, 4, 4, 4, 1024, True, True)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _units(s, dev):
+    import torch
+
+    from paper_2601_19362_b200 import worker as W
+
+    gen = torch.Generator(device=dev).manual_seed(0)
+    units = [W.init_unit(s, u, gen, dev) for u in range(len(W.unit_sizes(s)))]
+    for u in units:  # perturb norms / biases so their gradients are exercised
+        u += 0.01 * torch.randn(u.shape, generator=gen, device=dev)
+    return units
+
+
+def _run_queue(eng, s, queue, total, dev):
+    from paper_2601_19362_b200 import worker as W
+
+    wk = W.Worker(s, W.OdcComm(eng), dev, ce_chunk=256)
+    for mb in queue:
+        ntok = sum(LENS[i] for i in mb)
+        wk.microbatch(W.make_batch(LENS, mb, s.vocab, dev), ntok / total)
+
+
+def _rank(rank, world, port, q):
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from paper_2601_19362_b200 import worker as W
+        from paper_2601_19362_b200.engine import OdcEngine
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        s = _shape()
+        eng = OdcEngine(W.unit_sizes(s), rank=rank, world=world, device=0, push_mode="fixed", timeout_s=60)
+        for u, t in enumerate(_units(s, dev)):
+            eng.set_params(u, t)
+        torch.cuda.synchronize()
+        dist.barrier()
+        _run_queue(eng, s, GOLDEN[rank], float(sum(LENS)), dev)
+        eng.minibatch_end()
+        eng.check()
+        shards = [eng.read_grad_shard(u).cpu().numpy() for u in range(len(W.unit_sizes(s)))]  # by value
+        ranges = [eng.shard_range(u) for u in range(len(W.unit_sizes(s)))]
+        dist.barrier()
+        eng.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok", shards, ranges))
+    except Exception:
+        q.put((rank, traceback.format_exc(), None, None))
+
+
+def test_config0_two_ranks_on_one_gpu():
+    import torch
+    import torch.multiprocessing as mp
+    import torch.nn.functional as F
+
+    from paper_2601_19362_b200 import partition as P
+    from paper_2601_19362_b200 import worker as W
+    from paper_2601_19362_b200.engine import OdcEngine
+    from test_worker_gpu import ref_loss
+
+    plan = P.plan_flat("lb-mini", LENS, 2, 8, 2048, P.CostModel(1.0, 0.0, 1))
+    assert plan[0] == GOLDEN
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, msg, shards, ranges = q.get(timeout=300)
+        res[r] = (msg, shards, ranges)
+    for p in procs:
+        p.join(timeout=60)
+    bad = {r: m for r, (m, _, _) in res.items() if m != "ok"}
+    assert not bad, "\n".join(f"rank {r}:\n{m}" for r, m in bad.items())
+
+    s = _shape()
+    dev = torch.device("cuda", 0)
+    sizes = W.unit_sizes(s)
+    got = [torch.cat([torch.from_numpy(res[r][1][u]) for r in range(2)]) for u in range(len(sizes))]
+    for u in range(len(sizes)):
+        assert res[0][2][u][1] + res[1][2][u][1] == sizes[u]
+
+    # the same microbatches, in a different order, through one world=1 FIXED engine: identical bits
+    eng = OdcEngine(sizes, push_mode="fixed")
+    for u, t in enumerate(_units(s, dev)):
+        eng.set_params(u, t)
+    _run_queue(eng, s, GOLDEN[1][::-1] + GOLDEN[0], float(sum(LENS)), dev)
+    eng.minibatch_end()
+    eng.check()
+    diffs = []
+    for u in range(len(sizes)):
+        one = eng.read_grad_shard(u).cpu()
+        diffs.append(((got[u] - one).norm() / one.norm()).item())
+    eng.close()
+    print("two-rank vs one-rank rel-L2 per unit:", diffs)
+    # fixed-point sums are order-independent, but the per-microbatch gradients themselves come
+    # from bf16 kernels with atomically reduced parts (attention dq, norm/bias grads, split-K,
+    # embedding scatter-add): a 1-ulp fp32 difference that flips a bf16 rounding grows layer by
+    # layer down the backward (measured: 8e-8 on the last layer, 2e-3 on the embedding). A lost
+    # or doubled contribution of either rank would be O(0.3) (rank 0 holds 1/3 of the tokens).
+    assert max(diffs) < 1e-2, diffs
+
+    # fp32 autograd reference of the whole minibatch (token-weighted microbatch means)
+    ref_units = [t.to(torch.bfloat16).float().requires_grad_(True) for t in _units(s, dev)]
+    total = float(sum(LENS))
+    loss = 0.0
+    for queue in GOLDEN:
+        for mb in queue:
+            b = W.make_batch(LENS, mb, s.vocab, dev)
+            loss = loss + ref_loss(s, ref_units, b) * (sum(LENS[i] for i in mb) / total)
+    loss.backward()
+    for u in range(len(sizes)):
+        want = ref_units[u].grad.cpu()
+        cos = F.cosine_similarity(got[u], want, dim=0).item()
+        rel = ((got[u] - want).norm() / want.norm()).item()
+        print("unit", u, "cos", cos, "rel", rel)
+        assert cos > 0.995 and rel < 5e-2, (u, cos, rel)
