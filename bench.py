@@ -717,17 +717,20 @@ def main():
         # local HBM copy: read + write of the whole unit
         f_bytes = M * P2_BYTES_BF16 * 2
         roof = {"bound": "hbm", "achieved": round(f_bytes / (f_ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                "peak_kind": hbm_kind, "kernel": "copy_segments_kernel (odc_fetch)", "ms_per_launch": round(f_ms, 4),
+                "peak_kind": hbm_kind, "kernel": "fetch_tma_kernel (odc_fetch)", "ms_per_launch": round(f_ms, 4),
                 "bytes_per_launch": f_bytes, "traffic": None}
     else:
         f_bytes = (world - 1) * ((M + world - 1) // world) * P2_BYTES_BF16  # NVLink ingress per launch
         roof = {"bound": "nvlink", "achieved": round(f_bytes / (f_ms / 1e3) / 1e9, 1), "peak": NVLINK_NOMINAL_GBS,
-                "unit": "GB/s", "peak_kind": "nominal per-direction", "kernel": "copy_segments_kernel (odc_fetch)",
+                "unit": "GB/s", "peak_kind": "nominal per-direction", "kernel": "fetch_tma_kernel (odc_fetch)",
                 "ms_per_launch": round(f_ms, 4), "bytes_per_launch": f_bytes, "traffic": None}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     # N=1: read g + read-modify-write of the local fp32 shard (12 B/elem); N>1: NVLink egress
     push_bytes = M * 12 if world == 1 else (world - 1) * ((M + world - 1) // world) * P4_BYTES_F32
-    push_info = {"kernel": "push_red_kernel" if args.push_mode == "red" else "slot_accumulate_kernel",
+    big = (M + world - 1) // world >= (1 << 20)  # engine.cu: bulk reductions from 1M-element shards
+    push_kernel = {"red": "push_bulk_kernel<F32>" if big else "push_red_kernel", "fixed": "push_bulk_kernel<FIXED>",
+                   "slot": "slot_accumulate_kernel"}[args.push_mode]
+    push_info = {"kernel": push_kernel,
                  "ms_per_launch": round(p_ms, 4), "GBps": round(push_bytes / (p_ms / 1e3) / 1e9, 1)}
 
     # e2e through host buffers (reference-facing by-value I/O)
