@@ -296,6 +296,12 @@ __global__ void col_sum_kernel(const unsigned short* __restrict__ m, float* __re
 
 // ----------------------------------------------------------------- SwiGLU
 // one row per block-iteration, columns across the threads: no 64-bit division per element
+// The backward takes two 16-byte column groups per thread per step, every load
+// issued before any math (6 independent 16 B loads in flight instead of 3):
+// 350 -> 292 us at T=19K (4.86 -> 5.83 TB/s). The same change made the
+// forward slower (174 -> 190 us), so it keeps one group per step.
+constexpr int kGluThreads = 256;
+
 __global__ void swiglu_fwd_kernel(const uint4* __restrict__ gu, uint4* __restrict__ m, long long T, int fv) {
     for (long long t = blockIdx.x; t < T; t += gridDim.x) {
         const uint4* gr = gu + t * 2 * fv;
@@ -311,25 +317,47 @@ __global__ void swiglu_fwd_kernel(const uint4* __restrict__ gu, uint4* __restric
     }
 }
 
-__global__ void swiglu_bwd_kernel(const uint4* __restrict__ dm, const uint4* __restrict__ gu, uint4* __restrict__ dgu,
-                                  long long T, int fv) {
+__device__ __forceinline__ void swiglu_bwd8(const uint4& dv, const uint4& gv, const uint4& uv, uint4& dgo, uint4& duo) {
+    float d[8], g[8], u[8], dg[8], du[8];
+    unpack8(dv, d);
+    unpack8(gv, g);
+    unpack8(uv, u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float sg = __frcp_rn(1.f + __expf(-g[j]));
+        dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
+        du[j] = d[j] * g[j] * sg;
+    }
+    dgo = pack8(dg);
+    duo = pack8(du);
+}
+
+__global__ void __launch_bounds__(kGluThreads) swiglu_bwd_kernel(const uint4* __restrict__ dm,
+                                                                 const uint4* __restrict__ gu,
+                                                                 uint4* __restrict__ dgu, long long T, int fv) {
     for (long long t = blockIdx.x; t < T; t += gridDim.x) {
         const uint4* gr = gu + t * 2 * fv;
         const uint4* dr = dm + t * fv;
         uint4* orow = dgu + t * 2 * fv;
-        for (int c = threadIdx.x; c < fv; c += blockDim.x) {
-            float d[8], g[8], u[8], dg[8], du[8];
-            unpack8(dr[c], d);
-            unpack8(gr[c], g);
-            unpack8(gr[fv + c], u);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float sg = __frcp_rn(1.f + __expf(-g[j]));
-                dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
-                du[j] = d[j] * g[j] * sg;
+        for (int c = threadIdx.x; c < fv; c += 2 * kGluThreads) {
+            const int c2 = c + kGluThreads;
+            const bool two = c2 < fv;
+            const uint4 d0 = dr[c], g0 = gr[c], u0 = gr[fv + c];
+            uint4 d1 = d0, g1 = g0, u1 = u0;
+            if (two) {
+                d1 = dr[c2];
+                g1 = gr[c2];
+                u1 = gr[fv + c2];
             }
-            orow[c] = pack8(dg);
-            orow[fv + c] = pack8(du);
+            uint4 a, b;
+            swiglu_bwd8(d0, g0, u0, a, b);
+            orow[c] = a;
+            orow[fv + c] = b;
+            if (two) {
+                swiglu_bwd8(d1, g1, u1, a, b);
+                orow[c2] = a;
+                orow[fv + c2] = b;
+            }
         }
     }
 }
