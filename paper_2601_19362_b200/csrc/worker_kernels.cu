@@ -116,7 +116,7 @@ __global__ void rmsnorm_bwd_kernel(const uint4* __restrict__ dy, const uint4* __
 // Register-accumulator variant: lane l of every warp owns the uint4 columns l, l+32, .. (KMAX per lane), so
 // the dw partial of the rows a warp handles stays in registers; one shared-memory reduction per block at the end.
 template <int KMAX>
-__global__ void __launch_bounds__(256, 2) rmsnorm_bwd_reg_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
+__global__ void __launch_bounds__(256, KMAX > 4 ? 1 : 2) rmsnorm_bwd_reg_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
                                                                 const uint4* __restrict__ w, const float* __restrict__ rstd,
                                                                 const uint4* __restrict__ resid, uint4* __restrict__ out,
                                                                 float* __restrict__ dw, long long T, int dv) {
@@ -134,44 +134,45 @@ __global__ void __launch_bounds__(256, 2) rmsnorm_bwd_reg_kernel(const uint4* __
         const float r = rstd[row];
         const uint4* dyr = dy + row * dv;
         const uint4* xr = x + row * dv;
-        float dot = 0.f;
-        {  // pass 1: all loads of the row in flight, then the dot product
-            uint4 ra[KMAX], rb[KMAX];
+        const uint4* rr = resid ? resid + row * dv : nullptr;
+        // every load of the row (dy, x and the residual) in flight at once, kept in registers for both passes
+        uint4 ra[KMAX], rb[KMAX], rc[KMAX];
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                const int i = lane + 32 * k;
-                if (i < dv) {
-                    ra[k] = dyr[i];
-                    rb[k] = xr[i];
-                }
+        for (int k = 0; k < KMAX; ++k) {
+            const int i = lane + 32 * k;
+            if (i < dv) {
+                ra[k] = dyr[i];
+                rb[k] = xr[i];
+                if (rr) rc[k] = rr[i];
             }
+        }
+        float dot = 0.f;
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                const int i = lane + 32 * k;
-                if (i < dv) {
-                    float a[8], bb[8], g[8];
-                    unpack8(ra[k], a);
-                    unpack8(rb[k], bb);
-                    unpack8(__ldg(w + i), g);
+        for (int k = 0; k < KMAX; ++k) {
+            const int i = lane + 32 * k;
+            if (i < dv) {
+                float a[8], bb[8], g[8];
+                unpack8(ra[k], a);
+                unpack8(rb[k], bb);
+                unpack8(__ldg(w + i), g);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) dot += a[j] * g[j] * bb[j];
-                }
+                for (int j = 0; j < 8; ++j) dot += a[j] * g[j] * bb[j];
             }
         }
         const float c = warp_sum(dot) * r / d;
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) {  // pass 2: the row again (L1 hits), residual, output, dw partial
+        for (int k = 0; k < KMAX; ++k) {  // residual, output, dw partial from the registers
             const int i = lane + 32 * k;
             if (i < dv) {
                 float a[8], bb[8], g[8], o[8];
-                unpack8(dyr[i], a);
-                unpack8(xr[i], bb);
+                unpack8(ra[k], a);
+                unpack8(rb[k], bb);
                 unpack8(__ldg(w + i), g);
-                if (resid) unpack8(resid[row * dv + i], o);
+                if (rr) unpack8(rc[k], o);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float xh = bb[j] * r;
-                    o[j] = (resid ? o[j] : 0.f) + r * (a[j] * g[j] - xh * c);
+                    o[j] = (rr ? o[j] : 0.f) + r * (a[j] * g[j] - xh * c);
                     acc[k][j] += a[j] * xh;  // dw += dy * xhat
                 }
                 out[row * dv + i] = pack8(o);
