@@ -441,6 +441,16 @@ def run_sft(args):
                 "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": ncu_traffic("gemm::gemm2_kernel"),
                 "traffic_source": "profiles/r01/ncu_traffic.json (dram read+write per launch, ncu --set full)"}
     pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
+    # model FLOPs utilisation of the whole step: per sequence 6*P_nonembed*s (dense)
+    # + 6*L*d*s^2 (causal attention, fwd+bwd) + 6*V*d*s (LM head); recompute is not counted
+    step_flops = sum(6.0 * shape.nonembed_params * lens[i] + 6.0 * shape.layers * shape.d * float(lens[i]) ** 2
+                     + 6.0 * shape.vocab * shape.d * lens[i]
+                     for k in timed_steps for dv in plan_odc[k % len(plan_odc)] for mb in dv for i in mb)
+    model_tflops = step_flops / (res["ms"] / 1e3) / 1e12
+    mfu = {"model_tflops": round(model_tflops, 1), "per_gpu_tflops": round(model_tflops / world, 1),
+           "peak_per_gpu": tflops_peak, "frac": round(model_tflops / world / tflops_peak, 4),
+           "frac_vs_burst": round(model_tflops / world / tflops_burst, 4),
+           "flops": "6*P_nonembed*s + 6*L*d*s^2 + 6*V*d*s per sequence (SURVEY 8(d)); recompute not counted"}
     h2d = sum(16 * lens[i] + 8 + 16 * (shape.heads + shape.kv_heads) * ((lens[i] + 127) // 128)  # + attn work lists
               for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
     cpu = None
@@ -465,7 +475,7 @@ def run_sft(args):
                              "analytic_compute_only_speedup": round(pred[0], 4),
                              "analytic_bubble_odc_lbmini": round(pred[1], 4),
                              "analytic_bubble_fsdp_lbmicro": round(pred[2], 4)} if fs else None),
-                "roofline": roof, "fetch_push": comm, "clocks": clk.summary(),
+                "roofline": roof, "mfu": mfu, "fetch_push": comm, "clocks": clk.summary(),
                 "e2e": ({"value": round(e2e["tps"], 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / args.steps),
                          "d2h_bytes_per_step": 4, "loss": e2e["loss"],
                          "note": "token ids/labels/positions built on host per microbatch, copied H2D inside the "
