@@ -463,9 +463,12 @@ odc_status odc_w_rmsnorm_bwd(const void* dy, const void* x, const void* w, const
                              void* out, float* dw, std::int64_t T, int d, void* stream) {
     return odc::guard([&] {
         need(d % 8 == 0, "rmsnorm: d % 8 == 0");
-        const int blocks = static_cast<int>(std::min<long long>((T + 7) / 8, 148 * 4));
-        odc::count_launch();
         const int kmax = (d / 8 + 31) / 32;  // uint4 columns per lane
+        // register kernels: one wave of exactly the resident CTAs (1 per SM for KMAX > 4, else 2) — every
+        // extra CTA pays the dw reduction again (T=19K: 79 -> 60 us, T=4K: 39 -> 21 us vs 4 per SM)
+        const int grid_per_sm = kmax > 6 ? 4 : kmax > 4 ? 1 : 2;
+        const int blocks = static_cast<int>(std::min<long long>((T + 7) / 8, 148 * grid_per_sm));
+        odc::count_launch();
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         auto args = [&](auto kern) {
             kern<<<blocks, 256, d * sizeof(float), st>>>(static_cast<const uint4*>(dy), static_cast<const uint4*>(x),
