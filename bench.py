@@ -174,6 +174,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cpu_threads(elems):
+    """Host threads for the reference CPU sample: one independent FSDP unit per
+    thread, bounded by the cores this process may use and by host memory (a
+    ShardFabric<float> sample holds ~6 copies of the unit in fp32)."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        import psutil
+        mem = psutil.virtual_memory().available
+    except Exception:
+        mem = 16 << 30
+    per = max(1, 6 * 4 * int(elems))
+    return max(1, min(cores, int(os.environ.get("ODC_CPU_THREADS", "64")), int(0.5 * mem // per)))
+
+
 def cpu_reference_sample(world, elems, micro):
     """Times the reference's CPU fabric (ShardFabric<float>) on a bounded
     sample: one FSDP unit, `world` simulated ranks, each client fetching twice
@@ -185,10 +199,12 @@ def cpu_reference_sample(world, elems, micro):
     # same logical work, normalised to the B200 path's dtypes (bf16 fetch, fp32 push)
     bytes_equiv = world * (gathers * elems * P2_BYTES_BF16 + pushes * elems * P4_BYTES_F32)
     if R.available():
-        sec = R.fabric_seconds_f32(world, elems, gathers, pushes, 1)
+        thr = cpu_threads(elems)
+        sec = R.fabric_seconds_f32_mt(world, elems, gathers, pushes, 1, thr) / thr
         return sec, bytes_equiv, "reference", (f"ShardFabric<float>({world}, {elems}) from oracle/_ref: "
                                                 f"{world} clients x ({gathers} gather + {pushes} scatter_accumulate)"
-                                                f" + finalize_minibatch, one FSDP unit of one microbatch")
+                                                f" + finalize_minibatch, one FSDP unit of one microbatch; "
+                                                f"{thr} units on {thr} host threads, per-unit time = wall/{thr}")
     import numpy as np
 
     from oracle import odc_oracle as O
@@ -247,7 +263,9 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": args.workload, "model": shape.name, "world": world},
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": kind, "sample": sample},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s",
+                             "cores": cpu_threads(shape.layer_elems) if kind == "reference" else 1,
+                             "kind": kind, "sample": sample},
             "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -592,11 +610,12 @@ def cpu_tokens_baseline(lens, plan, steps, sizes, world, minibs=8, budget=32768,
     from oracle import refbind as R
 
     s, _, kind, sample = cpu_reference_sample(world, sizes[1], 1)
+    cores = cpu_threads(sizes[1]) if kind == "reference" else 1
     micro = sum(len(dv) for k in steps for dv in plan[k % len(plan)])
     t_plan = R.plan_seconds("lb-mini", lens, world, minibs, budget, 1.0, beta, 1) if R.available() else 0.0
     t = s * len(sizes) * micro / max(1, world) + t_plan * len(steps)
     toks = sum(lens[i] for k in steps for dv in plan[k % len(plan)] for mb in dv for i in mb)
-    return {"value": round(toks / t, 2), "unit": "tokens/s", "cores": 1, "kind": kind,
+    return {"value": round(toks / t, 2), "unit": "tokens/s", "cores": cores, "kind": kind,
             "sample": sample + f"; extrapolated x{len(sizes)} units x {micro} microbatches + plan()"}
 
 
@@ -768,7 +787,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s, b, kind, sample = cpu_reference_sample(1, M, 1)
-        cpu = {"value": round(b / s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": kind, "sample": sample}
+        cpu = {"value": round(b / s / 1e9, 4), "unit": "GB/s", "cores": cpu_threads(M) if kind == "reference" else 1,
+               "kind": kind, "sample": sample}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "odcsim/cost_model.hpp"
@@ -221,6 +222,29 @@ double ref_fabric_seconds_f32(int ranks, std::int64_t elems, int gathers_per_cli
     }
     auto t1 = std::chrono::steady_clock::now();
     return sink >= 0.0 ? std::chrono::duration<double>(t1 - t0).count() : -1.0;
+}
+
+// The same sample on `threads` host threads, each moving its own FSDP unit
+// through its own ShardFabric<float> (units are independent fabrics; one
+// fabric is not thread-safe, and the reference's threaded driver serialises
+// every client under one mutex, inc/primitives.hpp:296-303). Returns the wall
+// time for all `threads` units; per-unit time = wall / threads.
+double ref_fabric_seconds_f32_mt(int ranks, std::int64_t elems, int gathers_per_client,
+                                 int pushes_per_client, int iters, int threads) {
+    if (threads <= 1) return ref_fabric_seconds_f32(ranks, elems, gathers_per_client, pushes_per_client, iters);
+    std::vector<std::thread> pool;
+    std::vector<double> sec(static_cast<std::size_t>(threads), 0.0);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            sec[static_cast<std::size_t>(t)] =
+                ref_fabric_seconds_f32(ranks, elems, gathers_per_client, pushes_per_client, iters);
+        });
+    for (auto& th : pool) th.join();
+    auto t1 = std::chrono::steady_clock::now();
+    for (double v : sec)
+        if (v < 0.0) return -1.0;
+    return std::chrono::duration<double>(t1 - t0).count();
 }
 
 // Analytic compute-only runtimes (src/runtime.cpp:52-79) of a plan, for the

@@ -49,6 +49,8 @@ def lib() -> C.CDLL:
         L.ref_run_schedule_i64.restype = C.c_int64
         L.ref_fabric_seconds_f32.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int]
         L.ref_fabric_seconds_f32.restype = C.c_double
+        L.ref_fabric_seconds_f32_mt.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_fabric_seconds_f32_mt.restype = C.c_double
         L.ref_runtime.argtypes = [C.c_int, i64p, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_double,
                                   C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib = L
@@ -149,6 +151,11 @@ def run_schedule_i64(ranks, elems, pushes, seed):
 
 def fabric_seconds_f32(ranks, elems, gathers_per_client, pushes_per_client, iters) -> float:
     return lib().ref_fabric_seconds_f32(ranks, elems, gathers_per_client, pushes_per_client, iters)
+
+
+def fabric_seconds_f32_mt(ranks, elems, gathers_per_client, pushes_per_client, iters, threads) -> float:
+    """Wall seconds for `threads` independent units on `threads` host threads."""
+    return lib().ref_fabric_seconds_f32_mt(ranks, elems, gathers_per_client, pushes_per_client, iters, threads)
 
 
 def runtime(strategy, lens, devices, minibs, budget, alpha=1.0, beta=0.0, layers=1):
