@@ -496,7 +496,7 @@ def run_sft(args):
                 "roofline": roof, "mfu": mfu, "fetch_push": comm, "clocks": clk.summary(),
                 "e2e": ({"value": round(e2e["tps"], 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / args.steps),
                          "d2h_bytes_per_step": 4, "loss": e2e["loss"],
-                         "note": "token ids/labels/positions built on host per microbatch, copied H2D inside the "
+                         "note": "token ids/labels/positions built on host per microbatch, staged in pinned host memory and copied H2D (async) inside the "
                                  "timed region; loss read back D2H every step"} if e2e else None),
                 "cpu_baseline": cpu, "gpu_launches": res["launches"]}
         print(json.dumps(line), flush=True)

@@ -92,7 +92,8 @@ def attn_items(lens, H: int, device) -> torch.Tensor:
                 items.append((start, n, qt, h))
         start += n
     items.sort(key=lambda t: -t[2])
-    return torch.tensor(items, dtype=torch.int32).to(device, non_blocking=True)
+    t = torch.tensor(items, dtype=torch.int32)
+    return (t.pin_memory() if torch.device(device).type == "cuda" else t).to(device, non_blocking=True)
 
 
 def attn_fwd(q, k, v, items, scale):
@@ -128,7 +129,8 @@ def attn_bwd_items(lens, H: int, KV: int, device, sms: int = 148) -> torch.Tenso
             for h in range(KV):
                 items.append((st, n, kt, h, b, e, 0, 0))
     items.sort(key=lambda x: x[4] - x[5])
-    return torch.tensor(items, dtype=torch.int32).to(device, non_blocking=True)
+    t = torch.tensor(items, dtype=torch.int32)
+    return (t.pin_memory() if torch.device(device).type == "cuda" else t).to(device, non_blocking=True)
 
 
 def attn_bwd(q, k, v, o, dout, lse, items, scale):

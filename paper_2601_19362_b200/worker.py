@@ -257,10 +257,15 @@ def make_batch(lens: Sequence[int], sample_ids: Sequence[int], vocab: int, devic
         pos.append(torch.arange(n))
         cu.append(cu[-1] + n)
     T = cu[-1]
-    b = Batch(torch.cat(ids).to(device, non_blocking=True), torch.cat(labels).to(device, non_blocking=True),
-              torch.cat(pos).to(device, non_blocking=True),
-              torch.tensor(cu, dtype=torch.int32).to(device, non_blocking=True),
-              max(int(lens[s]) for s in sample_ids), T)
+    # pinned staging: the H2D copies are asynchronous (a pageable copy would
+    # drain the stream while the host builds the next tensor)
+    pin = torch.device(device).type == "cuda"
+
+    def h2d(t):
+        return (t.pin_memory() if pin else t).to(device, non_blocking=True)
+
+    b = Batch(h2d(torch.cat(ids)), h2d(torch.cat(labels)), h2d(torch.cat(pos)),
+              h2d(torch.tensor(cu, dtype=torch.int32)), max(int(lens[s]) for s in sample_ids), T)
     if heads:
         attach_attn_items(b, [int(lens[s]) for s in sample_ids], heads, device, kv_heads)
     return b

@@ -52,3 +52,29 @@ tot = sum(agg.values())
 print(f"total device time {tot / 1e3:.1f} ms; tokens {sum(lens[i] for dv in plan[1] for mb in dv for i in mb)}")
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:25]:
     print(f"{v / tot * 100:5.1f}%  {v / 1e3:8.2f} ms  n={cnt[k]:5d}  {k}")
+
+# Idle gaps on the device: union of all kernel intervals (every stream) vs the
+# profiled span; the largest gaps with the kernels either side of them.
+iv = sorted((e.time_range.start, e.time_range.end, e.name[:60]) for e in prof.events()
+            if e.device_type == torch.autograd.DeviceType.CUDA)
+if iv:
+    span = iv[-1][1] - iv[0][0]
+    busy, cur_s, cur_e, last = 0.0, iv[0][0], iv[0][1], iv[0][2]
+    gaps = []
+    for s, e, n in iv[1:]:
+        if s > cur_e:
+            busy += cur_e - cur_s
+            gaps.append((s - cur_e, last, n))
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+        if e >= cur_e:
+            last = n
+    busy += cur_e - cur_s
+    print(f"device span {span / 1e3:.1f} ms, busy (union) {busy / 1e3:.1f} ms, idle {(span - busy) / 1e3:.1f} ms "
+          f"in {len(gaps)} gaps")
+    hist = defaultdict(float)
+    for g, a_, b_ in gaps:
+        hist[(a_[:40], b_[:40])] += g
+    for (a_, b_), g in sorted(hist.items(), key=lambda x: -x[1])[:12]:
+        print(f"  {g / 1e3:7.2f} ms  after {a_!r} before {b_!r}")
