@@ -8,6 +8,7 @@
 //   col_sum            bias gradient (fp32 column sums)
 //   swiglu_fwd/bwd     m = silu(g) * u and its gradient
 //   ce_fwd_bwd         per row: online logsumexp, loss, dlogits = (softmax - onehot)*scale in place
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(kGluThreads) swiglu_bwd_kernel(const uint4* __
 // ------------------------------------------------------- cross entropy
 // one CTA per row; logits row overwritten by dlogits = (softmax - onehot) * scale
 constexpr int kCeThreads = 512;
+constexpr int kCeSmemDefault = 0;
 __global__ void __launch_bounds__(kCeThreads) ce_kernel(uint4* __restrict__ logits, const long long* __restrict__ labels,
                                                         long long rows, int vv, float scale, float* __restrict__ loss) {
     const long long row = blockIdx.x;
@@ -373,19 +375,19 @@ __global__ void __launch_bounds__(kCeThreads) ce_kernel(uint4* __restrict__ logi
     const long long lab = labels[row];
     __shared__ float red_m[kCeThreads / 32], red_s[kCeThreads / 32];
     __shared__ float s_lse;
+    // online (max, sum) per 16 B chunk: one max over the 8 values, one
+    // rescale, 8 exps, no data-dependent branches
     float mx = -INFINITY, sm = 0.f;
     for (int i = threadIdx.x; i < vv; i += kCeThreads) {
         float f[8];
         unpack8(L[i], f);
+        float cm = fmaxf(fmaxf(fmaxf(f[0], f[1]), fmaxf(f[2], f[3])), fmaxf(fmaxf(f[4], f[5]), fmaxf(f[6], f[7])));
+        const float m = fmaxf(mx, cm);
+        float cs = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (f[j] > mx) {
-                sm = sm * __expf(mx - f[j]) + 1.f;
-                mx = f[j];
-            } else {
-                sm += __expf(f[j] - mx);
-            }
-        }
+        for (int j = 0; j < 8; ++j) cs += __expf(f[j] - m);
+        sm = (mx == -INFINITY ? 0.f : sm * __expf(mx - m)) + cs;
+        mx = m;
     }
     // warp then block reduction of (max, sum)
 #pragma unroll
@@ -556,7 +558,15 @@ odc_status odc_w_ce_fwd_bwd(void* logits, const std::int64_t* labels, std::int64
         need(vocab % 8 == 0, "ce: vocab % 8 == 0");
         if (rows <= 0) return;
         odc::count_launch();
-        ce_kernel<<<static_cast<unsigned>(rows), kCeThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        // resident CTAs per SM bound the rows in flight (each row is re-read by
+        // the gradient pass: rows in flight x V x 2 B should fit in L2)
+        static const int smem = [] {
+            const char* e = std::getenv("ODC_CE_SMEM");
+            const int v = e ? std::atoi(e) : kCeSmemDefault;
+            if (v > 48 * 1024) cudaFuncSetAttribute(ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+            return v;
+        }();
+        ce_kernel<<<static_cast<unsigned>(rows), kCeThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
             static_cast<uint4*>(logits), reinterpret_cast<const long long*>(labels), rows,
             static_cast<int>(vocab / 8), scale, loss);
         ok(cudaGetLastError(), "ce");

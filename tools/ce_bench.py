@@ -1,0 +1,42 @@
+"""CE fwd+bwd kernel alone at one chunk (8,192 rows x Qwen vocab): time, HBM
+GB/s of the algorithmic traffic (read + write of the bf16 logits), and the
+loss / dlogits against a torch fp32 reference. ODC_CE_SMEM sets the dynamic
+shared memory per CTA (occupancy knob)."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2601_19362_b200 import fused as F  # noqa: E402
+
+R, V = int(sys.argv[1]) if len(sys.argv) > 1 else 8192, 151936
+g = torch.Generator(device="cuda").manual_seed(0)
+x = (torch.randn(R, V, device="cuda", generator=g) * 3).to(torch.bfloat16)
+lab = torch.randint(0, V, (R,), device="cuda", generator=g)
+lab[::7] = -100
+nv = int((lab >= 0).sum())
+loss = torch.zeros((), device="cuda")
+y = F.ce_fwd_bwd_(x.clone(), lab, 1.0 / nv, loss)
+ref = x.float().requires_grad_(True)
+rl = torch.nn.functional.cross_entropy(ref, lab, ignore_index=-100, reduction="sum") / nv
+rl.backward()
+err_l = abs(loss.item() / nv - rl.item()) / abs(rl.item())
+err_g = ((y.float() - ref.grad).abs().max() / ref.grad.abs().max()).item()
+bufs = [x.clone() for _ in range(3)]
+for b in bufs:
+    F.ce_fwd_bwd_(b, lab, 1.0 / nv, loss)
+torch.cuda.synchronize()
+a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ts = []
+for k in range(6):
+    buf = bufs[k % 3]
+    a.record()
+    F.ce_fwd_bwd_(buf, lab, 1.0 / nv, loss)
+    b_.record()
+    torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b_))
+ms = sorted(ts)[len(ts) // 2]
+print(json.dumps({"smem": os.environ.get("ODC_CE_SMEM", "default"), "rows": R, "ms": round(ms, 3),
+                  "GBps": round(2 * R * V * 2 / ms / 1e6, 1), "rel_err_loss": err_l, "rel_err_grad_max": err_g}))
