@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(kGluThreads) swiglu_bwd_kernel(const uint4* __
 // one CTA per row; logits row overwritten by dlogits = (softmax - onehot) * scale
 constexpr int kCeThreads = 512;
 constexpr int kCeSmemDefault = 0;
+constexpr int kCeUnroll = 1;  // 4 measured slower (1.27 vs 1.21 ms per 8K rows)
 __global__ void __launch_bounds__(kCeThreads) ce_kernel(uint4* __restrict__ logits, const long long* __restrict__ labels,
                                                         long long rows, int vv, float scale, float* __restrict__ loss) {
     const long long row = blockIdx.x;
@@ -378,7 +379,27 @@ __global__ void __launch_bounds__(kCeThreads) ce_kernel(uint4* __restrict__ logi
     // online (max, sum) per 16 B chunk: one max over the 8 values, one
     // rescale, 8 exps, no data-dependent branches
     float mx = -INFINITY, sm = 0.f;
-    for (int i = threadIdx.x; i < vv; i += kCeThreads) {
+    // kCeUnroll 16 B loads in flight per thread before any math
+    int i0 = threadIdx.x;
+    for (; i0 + (kCeUnroll - 1) * kCeThreads < vv; i0 += kCeUnroll * kCeThreads) {
+        uint4 q[kCeUnroll];
+#pragma unroll
+        for (int u = 0; u < kCeUnroll; ++u) q[u] = L[i0 + u * kCeThreads];
+#pragma unroll
+        for (int u = 0; u < kCeUnroll; ++u) {
+            float f[8];
+            unpack8(q[u], f);
+            const float cm = fmaxf(fmaxf(fmaxf(f[0], f[1]), fmaxf(f[2], f[3])),
+                                   fmaxf(fmaxf(f[4], f[5]), fmaxf(f[6], f[7])));
+            const float m = fmaxf(mx, cm);
+            float cs = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cs += __expf(f[j] - m);
+            sm = (mx == -INFINITY ? 0.f : sm * __expf(mx - m)) + cs;
+            mx = m;
+        }
+    }
+    for (int i = i0; i < vv; i += kCeThreads) {
         float f[8];
         unpack8(L[i], f);
         float cm = fmaxf(fmaxf(fmaxf(f[0], f[1]), fmaxf(f[2], f[3])), fmaxf(fmaxf(f[4], f[5]), fmaxf(f[6], f[7])));
@@ -418,7 +439,24 @@ __global__ void __launch_bounds__(kCeThreads) ce_kernel(uint4* __restrict__ logi
     __syncthreads();
     const float lse = s_lse;
     const float sc = lab >= 0 ? scale : 0.f;
-    for (int i = threadIdx.x; i < vv; i += kCeThreads) {
+    int i1 = threadIdx.x;
+    for (; i1 + (kCeUnroll - 1) * kCeThreads < vv; i1 += kCeUnroll * kCeThreads) {
+        uint4 q[kCeUnroll];
+#pragma unroll
+        for (int u = 0; u < kCeUnroll; ++u) q[u] = L[i1 + u * kCeThreads];
+#pragma unroll
+        for (int u = 0; u < kCeUnroll; ++u) {
+            float f[8];
+            unpack8(q[u], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const long long col = static_cast<long long>(i1 + u * kCeThreads) * 8 + j;
+                f[j] = (__expf(f[j] - lse) - (col == lab ? 1.f : 0.f)) * sc;
+            }
+            L[i1 + u * kCeThreads] = pack8(f);
+        }
+    }
+    for (int i = i1; i < vv; i += kCeThreads) {
         float f[8];
         unpack8(L[i], f);
 #pragma unroll
