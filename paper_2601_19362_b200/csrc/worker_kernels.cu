@@ -366,9 +366,9 @@ __global__ void __launch_bounds__(kGluThreads) swiglu_bwd_kernel(const uint4* __
 
 // ------------------------------------------------------- cross entropy
 // one CTA per row; logits row overwritten by dlogits = (softmax - onehot) * scale
-constexpr int kCeThreads = 512;
-constexpr int kCeSmemDefault = 0;
+constexpr int kCeThreadsDefault = 512;
 constexpr int kCeUnroll = 1;  // 4 measured slower (1.27 vs 1.21 ms per 8K rows)
+template <int kCeThreads>
 __global__ void __launch_bounds__(kCeThreads) ce_kernel(uint4* __restrict__ logits, const long long* __restrict__ labels,
                                                         long long rows, int vv, float scale, float* __restrict__ loss) {
     const long long row = blockIdx.x;
@@ -596,17 +596,21 @@ odc_status odc_w_ce_fwd_bwd(void* logits, const std::int64_t* labels, std::int64
         need(vocab % 8 == 0, "ce: vocab % 8 == 0");
         if (rows <= 0) return;
         odc::count_launch();
-        // resident CTAs per SM bound the rows in flight (each row is re-read by
-        // the gradient pass: rows in flight x V x 2 B should fit in L2)
-        static const int smem = [] {
-            const char* e = std::getenv("ODC_CE_SMEM");
-            const int v = e ? std::atoi(e) : kCeSmemDefault;
-            if (v > 48 * 1024) cudaFuncSetAttribute(ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
-            return v;
+        // threads per row-CTA (ODC_CE_THREADS 256/512/1024 for A/B). Fewer
+        // resident CTAs via extra shared memory (so the gradient pass re-reads
+        // from L2) measured slower (profiles/r01/ce_occupancy_ab.jsonl).
+        static const int nt = [] {
+            const char* e = std::getenv("ODC_CE_THREADS");
+            return e ? std::atoi(e) : kCeThreadsDefault;
         }();
-        ce_kernel<<<static_cast<unsigned>(rows), kCeThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-            static_cast<uint4*>(logits), reinterpret_cast<const long long*>(labels), rows,
-            static_cast<int>(vocab / 8), scale, loss);
+        auto go = [&](auto kern, int threads) {
+            kern<<<static_cast<unsigned>(rows), threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+                static_cast<uint4*>(logits), reinterpret_cast<const long long*>(labels), rows,
+                static_cast<int>(vocab / 8), scale, loss);
+        };
+        if (nt == 256) go(ce_kernel<256>, 256);
+        else if (nt == 1024) go(ce_kernel<1024>, 1024);
+        else go(ce_kernel<512>, 512);
         ok(cudaGetLastError(), "ce");
     });
 }

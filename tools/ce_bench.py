@@ -1,7 +1,7 @@
 """CE fwd+bwd kernel alone at one chunk (8,192 rows x Qwen vocab): time, HBM
 GB/s of the algorithmic traffic (read + write of the bf16 logits), and the
-loss / dlogits against a torch fp32 reference. ODC_CE_SMEM sets the dynamic
-shared memory per CTA (occupancy knob)."""
+loss / dlogits against a torch fp32 reference. ODC_CE_THREADS picks the CTA size
+(256/512/1024)."""
 import json
 import os
 import sys
@@ -38,5 +38,5 @@ for k in range(6):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b_))
 ms = sorted(ts)[len(ts) // 2]
-print(json.dumps({"smem": os.environ.get("ODC_CE_SMEM", "default"), "rows": R, "ms": round(ms, 3),
+print(json.dumps({"threads": os.environ.get("ODC_CE_THREADS", "512"), "rows": R, "ms": round(ms, 3),
                   "GBps": round(2 * R * V * 2 / ms / 1e6, 1), "rel_err_loss": err_l, "rel_err_grad_max": err_g}))
