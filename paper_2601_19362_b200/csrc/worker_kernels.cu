@@ -73,6 +73,48 @@ __global__ void rmsnorm_fwd_kernel(const uint4* __restrict__ x, const uint4* __r
     }
 }
 
+// Register variant for d <= 32*8*KMAX: every 16 B load of the row is issued
+// before the reduction and the row is normalised from registers (no re-read).
+template <int KMAX>
+__global__ void rmsnorm_fwd_reg_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w, uint4* __restrict__ y,
+                                       float* __restrict__ rstd, long long T, int dv, float eps) {
+    const int lane = threadIdx.x % 32;
+    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= T) return;
+    const uint4* xr = x + row * dv;
+    uint4 q[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int i = lane + 32 * k;
+        if (i < dv) q[k] = xr[i];
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        if (lane + 32 * k < dv) {
+            float f[8];
+            unpack8(q[k], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+        }
+    }
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss / (dv * 8) + eps);
+    if (lane == 0) rstd[row] = r;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int i = lane + 32 * k;
+        if (i < dv) {
+            float f[8], g[8];
+            unpack8(q[k], f);
+            unpack8(__ldg(w + i), g);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = f[j] * r * g[j];
+            y[row * dv + i] = pack8(f);
+        }
+    }
+}
+
 // one warp per row, 8 warps per block; dw partials in smem, then global atomics
 __global__ void rmsnorm_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x, const uint4* __restrict__ w,
                                    const float* __restrict__ rstd, const uint4* __restrict__ resid, uint4* __restrict__ out,
@@ -493,8 +535,15 @@ odc_status odc_w_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd,
     return odc::guard([&] {
         need(d % 8 == 0, "rmsnorm: d % 8 == 0");
         odc::count_launch();
-        rmsnorm_fwd_kernel<<<static_cast<int>((T + 7) / 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-            static_cast<const uint4*>(x), static_cast<const uint4*>(w), static_cast<uint4*>(y), rstd, T, d / 8, eps);
+        const int dv = d / 8;
+        auto go = [&](auto kern) {
+            kern<<<static_cast<int>((T + 7) / 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+                static_cast<const uint4*>(x), static_cast<const uint4*>(w), static_cast<uint4*>(y), rstd, T, dv, eps);
+        };
+        if (dv <= 32 * 6) go(rmsnorm_fwd_reg_kernel<6>);
+        else if (dv <= 32 * 16) go(rmsnorm_fwd_reg_kernel<16>);
+        else if (dv <= 32 * 20) go(rmsnorm_fwd_reg_kernel<20>);
+        else go(rmsnorm_fwd_kernel);
         ok(cudaGetLastError(), "rmsnorm_fwd");
     });
 }
