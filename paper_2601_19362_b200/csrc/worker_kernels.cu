@@ -252,12 +252,12 @@ __global__ void qkv_rope_fwd_kernel(const unsigned short* __restrict__ qkv, cons
         const long long t = idx / (static_cast<long long>(groups) * heads);
         const long long src = t * heads * hd + static_cast<long long>(h) * hd + gi * 8;
         float a[8], b[8];
-        unpack8(*reinterpret_cast<const uint4*>(qkv + src), a);
-        unpack8(*reinterpret_cast<const uint4*>(qkv + src + half), b);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(qkv + src)), a);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(qkv + src + half)), b);
         if (bias) {
             float ba[8], bb[8];
-            unpack8(*reinterpret_cast<const uint4*>(bias + h * hd + gi * 8), ba);
-            unpack8(*reinterpret_cast<const uint4*>(bias + h * hd + gi * 8 + half), bb);
+            unpack8(__ldg(reinterpret_cast<const uint4*>(bias + h * hd + gi * 8)), ba);
+            unpack8(__ldg(reinterpret_cast<const uint4*>(bias + h * hd + gi * 8 + half)), bb);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 a[j] += ba[j];
@@ -277,10 +277,20 @@ __global__ void qkv_rope_fwd_kernel(const unsigned short* __restrict__ qkv, cons
             off = (t * KV + (h - H - KV)) * hd;
         }
         if (h < H + KV) {
-            const float2* cs = table + pos[t] * half + gi * 8;
+            // 8 (cos, sin) pairs as four 16 B loads (the table row is 64 B aligned)
+            const float4* cs4 = reinterpret_cast<const float4*>(table + pos[t] * half + gi * 8);
+            float cc[8], sn[8];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 u = __ldg(cs4 + q4);
+                cc[2 * q4] = u.x;
+                sn[2 * q4] = u.y;
+                cc[2 * q4 + 1] = u.z;
+                sn[2 * q4 + 1] = u.w;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const float c = cs[j].x, s = cs[j].y;
+                const float c = cc[j], s = sn[j];
                 const float x1 = a[j], x2 = b[j];
                 a[j] = x1 * c - x2 * s;
                 b[j] = x2 * c + x1 * s;
@@ -311,10 +321,20 @@ __global__ void qkv_rope_bwd_kernel(const unsigned short* __restrict__ dq, const
         unpack8(*reinterpret_cast<const uint4*>(src + gi * 8), a);
         unpack8(*reinterpret_cast<const uint4*>(src + gi * 8 + half), b);
         if (h < H + KV) {
-            const float2* cs = table + pos[t] * half + gi * 8;
+            // 8 (cos, sin) pairs as four 16 B loads (the table row is 64 B aligned)
+            const float4* cs4 = reinterpret_cast<const float4*>(table + pos[t] * half + gi * 8);
+            float cc[8], sn[8];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 u = __ldg(cs4 + q4);
+                cc[2 * q4] = u.x;
+                sn[2 * q4] = u.y;
+                cc[2 * q4 + 1] = u.z;
+                sn[2 * q4 + 1] = u.w;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const float c = cs[j].x, s = cs[j].y;
+                const float c = cc[j], s = sn[j];
                 const float y1 = a[j], y2 = b[j];
                 a[j] = y1 * c + y2 * s;
                 b[j] = y2 * c - y1 * s;
