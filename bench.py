@@ -59,8 +59,6 @@ def parse():
     ap.add_argument("--trace", default="", help="write a Chrome trace (reference schema) of one extra ODC step")
     ap.add_argument("--cost", default="b200", choices=["b200", "flops"],
                     help="LB cost beta/alpha: FLOP ratio ('flops') or FLOP ratio x measured kernel-throughput ratio")
-    ap.add_argument("--attn", default="tcgen05", choices=["tcgen05", "flash"],
-                    help="attention kernels: own tcgen05 fwd+bwd, or flash-attn 2.8 (library)")
     ap.add_argument("--cache-params", action="store_true",
                     help="SURVEY 8(f)1: keep fetched units for the whole minibatch (one fetch per unit per step)")
     ap.add_argument("--model", default="qwen2.5-1.5b")
@@ -221,8 +219,78 @@ def cpu_reference_sample(world, elems, micro):
     return time.perf_counter() - t, bytes_equiv, "port", "oracle port (numpy), same sample"
 
 
+def ref_lengths(cap):
+    """The BASELINE workload from the REFERENCE's own generator (oracle/_ref:
+    generate_synthetic, src/workload.cpp:133-145), floored at 512 — the same
+    list the product's odc_generate_synthetic returns (bit-exact golden)."""
+    from oracle import refbind as R
+
+    return [max(512, x) for x in R.generate_synthetic(("lognormal", 8.0, 1.5), 2048, cap, 0)]
+
+
+def ref_plan(lens, world, minibs, budget, beta):
+    """LB-Mini plan from the reference's own plan() (solutions_to_json):
+    per step, per device, the microbatches' token sums."""
+    from oracle import refbind as R
+
+    js = json.loads(R.plan_json("lb-mini", lens, world, minibs, budget, 1.0, beta, 1))
+    return [[[mb["token_sum"] for mb in dev] for dev in st["per_device"]] for st in js["steps"]]
+
+
+def sft_config(args, shape, world, beta):
+    """The bench line's `config` — a function of the arguments only, so both
+    arms (odc and --impl reference) print the identical dict."""
+    return {"workload": "odc_sft", "model": shape.name, "plan": "lb-mini (odc) / lb-micro (fsdp)",
+            "minibs_per_rank": args.minibs, "budget_tokens": args.cap,
+            "lengths": f"lognormal(8,1.5) n=2048 cap={args.cap} seed=0, floor 512",
+            "recompute": args.recompute, "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
+            "cost_beta_over_alpha": round(beta, 1), "cost_model": args.cost, "cache_params": args.cache_params,
+            "attention": "tcgen05", "l2": "inputs > L2 (GBs of activations/units), no flush"}
+
+
+class RefStepTimer:
+    """The reference's CPU implementation of one ODC step, measured: every
+    FSDP unit at its true size (embedding + L layers) as a ShardFabric<float>
+    of `world` simulated ranks from oracle/_ref; per step each client gathers
+    every unit twice and scatter_accumulates it once per microbatch of its
+    LB-Mini queue, then finalize_minibatch per unit. Units run in parallel on
+    host threads (one fabric per thread at a time: it is not thread-safe)."""
+
+    def __init__(self, world, unit_sizes, threads):
+        from oracle import refbind as R
+
+        self.world, self.threads = world, threads
+        self.step = R.RefStep(world, unit_sizes)
+
+    def run(self, plan_step):
+        return self.step.run([len(dev) for dev in plan_step], self.threads)
+
+    def close(self):
+        self.step.close()
+
+
+def ref_threads(world, unit_sizes):
+    """Host threads for the reference step: every core this process may use,
+    bounded by host memory (each thread's two live gather copies of the
+    largest unit) and ODC_CPU_THREADS."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        import psutil
+        mem = psutil.virtual_memory().available
+    except Exception:
+        mem = 16 << 30
+    resident = 4 * sum(unit_sizes) * (2 + world)  # params + grads + ranks x slot shards, fp32
+    per = 8 * max(unit_sizes)
+    room = max(1, int((0.8 * mem - resident) // per))
+    return max(1, min(cores, int(os.environ.get("ODC_CPU_THREADS", "256")), room))
+
+
 def run_reference(args):
-    from paper_2601_19362_b200.shapes import SHAPES
+    """--impl reference: the reference's own CPU path of the ODC step, timed on
+    host cores. Everything comes from oracle/_ref (the unmodified reference
+    built by oracle/Makefile): workload lengths, the LB-Mini plan, and the
+    ShardFabric<float> data path; nothing of the product is loaded."""
+    from paper_2601_19362_b200.shapes import SHAPES  # pure-Python model constants
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -230,25 +298,50 @@ def run_reference(args):
     shape = SHAPES[args.model]
     world = args.gpus
     if args.workload == "sft":
-        from paper_2601_19362_b200 import partition as P
-        from paper_2601_19362_b200 import worker as W
+        from oracle import refbind as R
 
-        lens = workload_lengths(args.cap)
-        plan = P.plan_flat("lb-mini", lens, world, args.minibs, args.cap, P.CostModel(1.0, shape.beta_over_alpha(), 1))
-        sizes = W.unit_sizes(shape)
-        for k in range(args.warmup):
-            cpu_tokens_baseline(lens, plan, [k], sizes, world, args.minibs, args.cap, shape.beta_over_alpha())
+        if not R.available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (no /root/reference at build)"}))
+            return
+        beta = shape.beta_over_alpha_b200() if args.cost == "b200" else shape.beta_over_alpha()
+        lens = ref_lengths(args.cap)
+        t_plan0 = time.perf_counter()
+        plan = ref_plan(lens, world, args.minibs, args.cap, beta)
+        t_plan = time.perf_counter() - t_plan0
+        sizes = shape.unit_sizes()
+        thr = ref_threads(world, sizes)
+        timer = RefStepTimer(world, sizes, thr)
+        budget_s = float(os.environ.get("ODC_REF_BUDGET_S", "300"))
         t0 = time.perf_counter()
-        vals = [cpu_tokens_baseline(lens, plan, [args.warmup + k], sizes, world, args.minibs, args.cap,
-                                    shape.beta_over_alpha()) for k in range(args.steps)]
-        wall = time.perf_counter() - t0
-        tps = sum(v["value"] for v in vals) / len(vals)
+        t_first = timer.run(plan[0])  # warm-up 1: slot allocation / first-touch page faults
+        warm = 1
+        while warm < args.warmup and (time.perf_counter() - t0) + (args.warmup - warm + args.steps) * t_first < budget_s:
+            timer.run(plan[warm % len(plan)])
+            warm += 1
+        secs, toks, n = [], 0, 0
+        for k in range(args.warmup, args.warmup + args.steps):
+            if secs and (time.perf_counter() - t0) + sum(secs) / len(secs) > budget_s:
+                break  # bounded sample: the remaining steps would exceed the time budget
+            st = plan[k % len(plan)]
+            secs.append(timer.run(st) + t_plan / len(plan))  # + the reference plan() share of one step
+            toks += sum(sum(dev) for dev in st)
+        timer.close()
+        total = sum(secs)
+        tps = toks / total
+        sample = (f"ShardFabric<float>({world}, M) from oracle/_ref for every FSDP unit at its true size "
+                  f"({len(sizes)} units: {sizes[0]:,} + {len(sizes) - 1} x {sizes[1]:,} elements); per step every "
+                  f"client gathers each unit 2x and scatter_accumulates it 1x per microbatch of its LB-Mini queue "
+                  f"(reference plan()), then finalize_minibatch per unit; units in parallel on {thr} host threads; "
+                  f"{len(secs)} of {args.steps} steps measured (budget {budget_s:.0f} s), warmup {warm}")
         line = {"metric": METRIC, "impl": "reference", "value": round(tps, 2), "unit": "tokens/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "odc_sft", "model": shape.name, "world": world},
-                "cpu_baseline": {**vals[0], "value": round(tps, 2)},
-                "e2e": {"value": round(tps, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "steps": args.steps, "warmup": args.warmup, "steps_measured": len(secs), "warmup_run": warm,
+                "ms_per_step": round(total / len(secs) * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": sft_config(args, shape, world, beta),
+                "cpu_baseline": {"value": round(tps, 2), "unit": "tokens/s", "cores": thr, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": round(tps, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "plan_seconds": round(t_plan, 4), "tokens_timed": toks}
         print(json.dumps(line), flush=True)
         return
     for _ in range(args.warmup):
@@ -354,8 +447,8 @@ def run_sft(args):
         return sum(lens[i] for dv in plan[k % len(plan)] for mb in dv for i in mb)
 
     def run_arm(comm, plan, resident: bool, record=False, clocks=None):
-        worker = W.Worker(shape, comm, dev, cache_params=args.cache_params and comm.name == "odc", attn=args.attn,
-                          recompute=recompute)
+        worker = W.Worker(shape, comm, dev, cache_params=args.cache_params and comm.name == "odc",
+                          recompute=recompute, max_positions=max(65536, args.cap))
         chk = eng.check if comm.name == "odc" else comm.local.check
         stream = torch.cuda.current_stream()
 
@@ -473,20 +566,14 @@ def run_sft(args):
               for k in timed_steps for mb in plan_odc[k % len(plan_odc)][rank] for i in mb)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_tokens_baseline(lens, plan_odc, timed_steps, sizes, world, args.minibs, budget, beta)
+        cpu = cpu_step_baseline(args, shape, world, beta, timed_steps)
     if rank == 0:
         line = {"metric": METRIC, "value": round(res["tps"], 1), "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"] / args.steps, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (random-init weights, seeded random token ids of the workload lengths)",
-                "config": {"workload": "odc_sft", "model": shape.name, "plan": "lb-mini (odc) / lb-micro (fsdp)",
-                           "minibs_per_rank": args.minibs, "budget_tokens": budget,
-                           "lengths": f"lognormal(8,1.5) n=2048 cap={args.cap} seed=0, floor 512",
-                           "recompute": recompute,
-                           "push_mode": args.push_mode, "parallelism": f"odc-dp{world}",
-                           "cost_beta_over_alpha": round(beta, 1), "cost_model": args.cost,
-                           "cache_params": args.cache_params, "attention": args.attn,
-                           "tokens_timed": res["tokens"], "l2": "inputs > L2 (GBs of activations/units), no flush"},
+                "config": sft_config(args, shape, world, beta),
+                "recompute_resolved": recompute, "tokens_timed": res["tokens"],
                 "idle_fraction": round(res["idle"], 4),
                 "idle_note": "1 - sum(busy)/(N*T), busy = device time from step start to the minibatch barrier",
                 "vs_fsdp": ({"fsdp_tokens_per_s": round(fs["tps"], 1), "speedup": round(res["tps"] / fs["tps"], 4),
@@ -602,21 +689,36 @@ class _Null:
         return False
 
 
-def cpu_tokens_baseline(lens, plan, steps, sizes, world, minibs=8, budget=32768, beta=30467.0):
-    """Reference CPU path of one step, extrapolated from a bounded sample: the
-    reference fabric (ShardFabric<float>) moving one FSDP layer unit for one
-    microbatch (2 gathers + 1 scatter_accumulate per client + finalize), times
-    units x microbatches of the step, plus the reference plan() time."""
+def cpu_step_baseline(args, shape, world, beta, steps, budget_s=30.0):
+    """cpu_baseline of the GPU arm (rank 0, N=1): the reference's CPU path of
+    the same step (RefStepTimer: oracle/_ref ShardFabric<float> over every unit
+    at its true size, for every microbatch of the reference LB-Mini plan),
+    measured on host cores over a bounded sample of the timed steps (one
+    untimed warm-up step, then timed steps while they fit ~budget_s)."""
     from oracle import refbind as R
 
-    s, _, kind, sample = cpu_reference_sample(world, sizes[1], 1)
-    cores = cpu_threads(sizes[1]) if kind == "reference" else 1
-    micro = sum(len(dv) for k in steps for dv in plan[k % len(plan)])
-    t_plan = R.plan_seconds("lb-mini", lens, world, minibs, budget, 1.0, beta, 1) if R.available() else 0.0
-    t = s * len(sizes) * micro / max(1, world) + t_plan * len(steps)
-    toks = sum(lens[i] for k in steps for dv in plan[k % len(plan)] for mb in dv for i in mb)
-    return {"value": round(toks / t, 2), "unit": "tokens/s", "cores": cores, "kind": kind,
-            "sample": sample + f"; extrapolated x{len(sizes)} units x {micro} microbatches + plan()"}
+    if not R.available():
+        return None
+    lens = ref_lengths(args.cap)
+    t0 = time.perf_counter()
+    plan = ref_plan(lens, world, args.minibs, args.cap, beta)
+    t_plan = time.perf_counter() - t0
+    sizes = shape.unit_sizes()
+    thr = ref_threads(world, sizes)
+    timer = RefStepTimer(world, sizes, thr)
+    timer.run(plan[steps[0] % len(plan)])
+    secs, toks = [], 0
+    for k in steps:
+        if secs and sum(secs) + sum(secs) / len(secs) > budget_s:
+            break
+        st = plan[k % len(plan)]
+        secs.append(timer.run(st) + t_plan / len(plan))
+        toks += sum(sum(dev) for dev in st)
+    timer.close()
+    return {"value": round(toks / sum(secs), 2), "unit": "tokens/s", "cores": thr, "kind": "reference",
+            "sample": (f"{len(secs)} measured step(s) of the reference CPU path (oracle/_ref ShardFabric<float>, "
+                       f"{len(sizes)} units at true size, every microbatch of the reference LB-Mini plan: 2 gathers + "
+                       f"1 scatter_accumulate per unit per microbatch, finalize per unit, + plan()); {thr} host threads")}
 
 
 def main():

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ODC_ABI_VERSION 4
+#define ODC_ABI_VERSION 5
 
 typedef enum {
     ODC_OK = 0,
@@ -44,7 +44,8 @@ typedef enum {
     ODC_ERR_STATE = 6,      /* StateError                     inc/types.hpp:40-43 */
     ODC_ERR_MODE = 7,       /* ModeError                      inc/types.hpp:29-33 */
     ODC_ERR_CUDA = 8,       /* CUDA runtime failure (no reference counterpart) */
-    ODC_ERR_TIMEOUT = 9     /* device barrier watchdog fired (no reference counterpart) */
+    ODC_ERR_TIMEOUT = 9,    /* device barrier watchdog fired (no reference counterpart) */
+    ODC_ERR_RANGE = 10      /* FIXED push: a contribution saturated the int64 fixed-point range (no reference counterpart) */
 } odc_status;
 
 typedef enum { ODC_I64 = 0, ODC_F64 = 1, ODC_F32 = 2, ODC_BF16 = 3 } odc_dtype;
@@ -166,7 +167,12 @@ odc_status odc_push(odc_ctx_t ctx, int layer, const void* grad_full, int grad_dt
 odc_status odc_push_slice(odc_ctx_t ctx, int layer, int target, int64_t offset, const float* payload,
                           int64_t n, float weight, void* stream);
 /* (a8) minibatch barrier: signal every owner, wait for every client, then
- * (slot mode) reduce the per-source slots in rank order into the grad shard. */
+ * (slot mode) reduce the per-source slots in rank order into the grad shard,
+ * (fixed mode) convert the int64 sums into it. The grad shards then hold the
+ * minibatch's sums until the next AdamW step or the rank's next fetch / push /
+ * minibatch_end, which consume (zero) them like take_grads (:144-148): read
+ * them with odc_read_grad_shard before (stream-ordered) that next call.
+ * Peers' pushes of the next minibatch wait device-side for that drain. */
 odc_status odc_minibatch_end(odc_ctx_t ctx, void* stream);
 /* read this rank's accumulated fp32 grad shard of `layer` (len = shard_len) */
 odc_status odc_read_grad_shard(odc_ctx_t ctx, int layer, float* dst, void* stream);
@@ -177,11 +183,15 @@ typedef struct {
     int step; /* 1-based, for bias correction */
 } odc_adam_cfg;
 /* (a19) fused AdamW over every owned shard (fp32 master/m/v, bf16 shard out),
- * zeroes the grad shards, then publishes the new parameter epoch. In slot
- * mode the rank-order slot reduce is fused into the same kernel. */
+ * zeroes the grad shards, then publishes the new parameter epoch. (The slot
+ * mode's rank-order reduce already ran in odc_minibatch_end.) */
 odc_status odc_adam_step(odc_ctx_t ctx, const odc_adam_cfg* cfg, void* stream);
-/* host check of the device error word (watchdog); blocks on `stream` */
+/* host check of the device error word; blocks on `stream`. ODC_ERR_TIMEOUT
+ * (watchdog) or ODC_ERR_RANGE (FIXED push saturation / NaN) */
 odc_status odc_ctx_check(odc_ctx_t ctx, void* stream);
+/* raw sticky device flags: bit0 timeout, bit1 FIXED range error,
+ * bit2 FIXED underflow warning (a nonzero w*g rounded to 0); blocks on `stream` */
+odc_status odc_ctx_flags(odc_ctx_t ctx, uint64_t* flags, void* stream);
 /* current minibatch epoch (number of completed odc_minibatch_end calls) */
 int64_t odc_ctx_epoch(odc_ctx_t ctx);
 

@@ -11,6 +11,8 @@
 //   * timing of gather / scatter_accumulate / finalize on host cores
 // Nothing in the product (paper_2601_19362_b200/, include/) links this file.
 
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -245,6 +247,104 @@ double ref_fabric_seconds_f32_mt(int ranks, std::int64_t elems, int gathers_per_
     for (double v : sec)
         if (v < 0.0) return -1.0;
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// ---------------------------------------------------------------------------
+// One ODC minibatch step of the reference's CPU path, measured (bench.py
+// --impl reference and the GPU arm's cpu_baseline): every FSDP unit at its
+// true size is one ShardFabric<float> (one fabric = one unit's gradient
+// space, inc/primitives.hpp:158-159) with `ranks` simulated ranks. For every
+// microbatch of client c in the step (the LB-Mini plan): gather the unit
+// twice (forward + backward re-fetch, inc/primitives.hpp:177-179) and
+// scatter_accumulate its gradient once (:181-188); then finalize_minibatch
+// (:199-203) once per unit. Units are independent fabrics, so `threads` host
+// threads take units off a shared queue (largest first); one fabric is only
+// ever touched by one thread (it is not thread-safe).
+struct RefStep {
+    int ranks = 1;
+    std::vector<std::int64_t> elems;
+    std::vector<ShardFabric<float>*> fabs;
+    std::vector<std::vector<float>> grads;  // one read-only gradient per unit size
+    std::vector<int> grad_of;
+};
+
+void* ref_step_new(int ranks, int n_units, const std::int64_t* elems) {
+    try {
+        auto* h = new RefStep();
+        h->ranks = ranks;
+        for (int u = 0; u < n_units; ++u) {
+            h->elems.push_back(elems[u]);
+            auto* f = new ShardFabric<float>(ranks, elems[u]);
+            f->set_params("unit", std::vector<float>(static_cast<std::size_t>(elems[u]), 0.01f));
+            h->fabs.push_back(f);
+            int g = -1;
+            for (std::size_t k = 0; k < h->grads.size(); ++k)
+                if (static_cast<std::int64_t>(h->grads[k].size()) == elems[u]) g = static_cast<int>(k);
+            if (g < 0) {
+                h->grads.emplace_back(static_cast<std::size_t>(elems[u]), 1e-3f);
+                g = static_cast<int>(h->grads.size()) - 1;
+            }
+            h->grad_of.push_back(g);
+        }
+        return h;
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void ref_step_free(void* hv) {
+    auto* h = static_cast<RefStep*>(hv);
+    if (!h) return;
+    for (auto* f : h->fabs) delete f;
+    delete h;
+}
+
+// micro[c] = microbatches of client c in this step. Returns wall seconds
+// (negative on failure).
+double ref_step_run(void* hv, const int* micro, int threads) {
+    auto* h = static_cast<RefStep*>(hv);
+    if (!h) return -1.0;
+    const int n = static_cast<int>(h->fabs.size());
+    std::vector<int> order(static_cast<std::size_t>(n));
+    for (int u = 0; u < n; ++u) order[static_cast<std::size_t>(u)] = u;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return h->elems[static_cast<std::size_t>(a)] > h->elems[static_cast<std::size_t>(b)];
+    });
+    std::atomic<int> next{0};
+    std::atomic<bool> failed{false};
+    std::vector<double> sink(static_cast<std::size_t>(std::max(1, threads)), 0.0);
+    auto work = [&](int t) {
+        try {
+            for (int i = next++; i < n; i = next++) {
+                const int u = order[static_cast<std::size_t>(i)];
+                ShardFabric<float>& f = *h->fabs[static_cast<std::size_t>(u)];
+                const std::vector<float>& g = h->grads[static_cast<std::size_t>(h->grad_of[static_cast<std::size_t>(u)])];
+                const float w = 1.0f / static_cast<float>(h->ranks);
+                for (int c = 0; c < h->ranks; ++c)
+                    for (int m = 0; m < micro[c]; ++m) {
+                        sink[static_cast<std::size_t>(t)] += f.gather(c, "unit").back();  // forward fetch
+                        sink[static_cast<std::size_t>(t)] += f.gather(c, "unit").back();  // backward re-fetch
+                        f.scatter_accumulate(c, g, w);                                     // gradient push
+                    }
+                auto shards = f.finalize_minibatch();
+                sink[static_cast<std::size_t>(t)] += shards.front().empty() ? 0.0 : shards.front().front();
+            }
+        } catch (...) {
+            failed = true;
+        }
+    };
+    auto t0 = std::chrono::steady_clock::now();
+    if (threads <= 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+        for (auto& th : pool) th.join();
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    double s = 0.0;
+    for (double v : sink) s += v;
+    return (failed || s < 0.0) ? -1.0 : std::chrono::duration<double>(t1 - t0).count();
 }
 
 // Analytic compute-only runtimes (src/runtime.cpp:52-79) of a plan, for the

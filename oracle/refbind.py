@@ -51,6 +51,11 @@ def lib() -> C.CDLL:
         L.ref_fabric_seconds_f32.restype = C.c_double
         L.ref_fabric_seconds_f32_mt.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int]
         L.ref_fabric_seconds_f32_mt.restype = C.c_double
+        L.ref_step_new.argtypes = [C.c_int, C.c_int, i64p]
+        L.ref_step_new.restype = C.c_void_p
+        L.ref_step_free.argtypes = [C.c_void_p]
+        L.ref_step_run.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.c_int]
+        L.ref_step_run.restype = C.c_double
         L.ref_runtime.argtypes = [C.c_int, i64p, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_double,
                                   C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib = L
@@ -166,3 +171,31 @@ def runtime(strategy, lens, devices, minibs, budget, alpha=1.0, beta=0.0, layers
     if rc != 0:
         raise RefError(rc, "runtime failed")
     return tot.value, bub.value
+
+
+class RefStep:
+    """The reference CPU path of one ODC minibatch step (ref_driver.cpp
+    ref_step_*): one ShardFabric<float> per FSDP unit at its true size; per
+    step, every client gathers each unit twice and scatter_accumulates once per
+    microbatch, then finalize_minibatch. run() returns measured wall seconds."""
+
+    def __init__(self, ranks: int, unit_elems: Sequence[int]):
+        arr, p = _i64(unit_elems)
+        self.ranks = ranks
+        self.h = lib().ref_step_new(ranks, len(arr), p)
+        if not self.h:
+            raise RefError(9, "ref_step_new failed (host memory?)")
+
+    def run(self, micro_per_client: Sequence[int], threads: int) -> float:
+        m = (C.c_int * self.ranks)(*[int(x) for x in micro_per_client])
+        t = lib().ref_step_run(self.h, m, int(threads))
+        if t < 0:
+            raise RefError(9, "ref_step_run failed")
+        return t
+
+    def close(self):
+        if self.h:
+            lib().ref_step_free(self.h)
+            self.h = None
+
+    __del__ = close

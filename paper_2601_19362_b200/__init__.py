@@ -8,7 +8,7 @@ reference's interface (primitives, partition) plus the multi-GPU engine.
 """
 from . import errors
 from .errors import (BarrierTimeout, DeviceError, InfeasibleError, InvariantError, ModeError, ParamError,
-                     ProtocolError, StateError)
+                     ProtocolError, RangeError, StateError)
 
 __all__ = ["errors", "ParamError", "InfeasibleError", "InvariantError", "ProtocolError", "StateError", "ModeError",
-           "DeviceError", "BarrierTimeout"]
+           "DeviceError", "BarrierTimeout", "RangeError"]

@@ -13,7 +13,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ODC_LIB_PATH") or os.path.join(PKG, "lib", "libodc.so")  # override: A/B variant builds
 
 ODC_OK, ODC_ERR_PARAM, ODC_ERR_INFEASIBLE, ODC_ERR_INVARIANT = 0, 2, 3, 4
-ODC_ERR_PROTOCOL, ODC_ERR_STATE, ODC_ERR_MODE, ODC_ERR_CUDA, ODC_ERR_TIMEOUT = 5, 6, 7, 8, 9
+ODC_ERR_PROTOCOL, ODC_ERR_STATE, ODC_ERR_MODE, ODC_ERR_CUDA, ODC_ERR_TIMEOUT, ODC_ERR_RANGE = 5, 6, 7, 8, 9, 10
+ODC_FLAG_TIMEOUT, ODC_FLAG_FIXED_RANGE, ODC_FLAG_FIXED_UNDERFLOW = 1, 2, 4
 ODC_I64, ODC_F64, ODC_F32, ODC_BF16 = 0, 1, 2, 3
 ODC_PUSH_RED, ODC_PUSH_SLOT, ODC_PUSH_FIXED = 0, 1, 2
 ODC_FIXED_FRAC_BITS_DEFAULT = 40
@@ -70,6 +71,7 @@ SIGNATURES = {
     "odc_read_master_shard": (C.c_int, [vp, C.c_int, vp, vp]),
     "odc_adam_step": (C.c_int, [vp, C.POINTER(OdcAdamCfg), vp]),
     "odc_ctx_check": (C.c_int, [vp, vp]),
+    "odc_ctx_flags": (C.c_int, [vp, C.POINTER(C.c_uint64), vp]),
     "odc_ctx_epoch": (C.c_int64, [vp]),
     "odc_copy_segments": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), i64p, C.c_int, vp]),
     "odc_l2_flush": (C.c_int, [vp, i64, vp]),
@@ -110,7 +112,7 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.odc_abi_version() != 4:
+        if L.odc_abi_version() != 5:
             raise ImportError("libodc.so ABI version mismatch")
         _lib = L
     return _lib

@@ -5,6 +5,7 @@
 //
 //   [flags page 4 KB]  done[r] u64 (written by client r at the barrier),
 //                      param_epoch u64 (owner publishes after AdamW), err u64
+//                      (bit mask), drain_epoch u64 (push-target reuse gate)
 //   per FSDP unit l, this rank's owned shard (block_l = ceil(M_l / N)):
 //     param  bf16 [block+8]  stored at pad = begin % 8   (co-aligned with the
 //     grad   f32  [block+4]  stored at pad = begin % 4    caller's full-layer
@@ -25,14 +26,20 @@
 //
 // Ordering protocol (all device-side, sys scope):
 //   * fetch of owner r's shard waits param_epoch[r] >= adams completed here;
-//   * RED push into owner r waits the same gate (its grad shard was zeroed by
-//     that AdamW); SLOT push waits every owner (they finished reading slots);
-//   * minibatch_end: st.release.sys done[rank] into every owner, then waits
-//     ld.acquire.sys done[c] >= epoch for every client c;
+//   * every push into owner r waits drain_epoch[r] >= minibatches completed
+//     here: the owner has consumed what the previous minibatch left in its
+//     push target and published that with st.release.sys:
+//       RED    grad shard zeroed — by AdamW, or (no AdamW in between) by the
+//              owner's first ODC call of the next minibatch, after the caller
+//              read the shard (finalize_minibatch returns + zeroes, :144-148);
+//       SLOT   the owner's rank-order reduce of every client's slot finished
+//              (a client's first push of a unit overwrites its slot);
+//       FIXED  int64 sums converted to the fp32 grad shard and zeroed, right
+//              after the barrier;
+//     so correctness never depends on an AdamW step between minibatches;
+//   * minibatch_end: fence.acq_rel.sys, st.release.sys done[rank] into every
+//     owner, then waits ld.acquire.sys done[c] >= epoch for every client c;
 //   * AdamW then st.release.sys param_epoch = ++adams.
-//   * FIXED push into owner r waits acc_epoch[r] >= minibatches completed
-//     here: the owner converts its int64 sums to the fp32 grad shard and
-//     zeroes them right after the barrier, then publishes acc_epoch.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -65,7 +72,7 @@ constexpr std::int64_t kFlagsBytes = 4096;
 constexpr std::int64_t kDoneOff = 0;
 constexpr std::int64_t kEpochOff = 1024;
 constexpr std::int64_t kErrOff = 2048;
-constexpr std::int64_t kAccEpochOff = 3072;  // FIXED mode: minibatch whose accumulator the owner has drained
+constexpr std::int64_t kDrainOff = 3072;  // last minibatch whose push target the owner has consumed
 constexpr std::uint64_t kBlobMagic = 0x4f44433142323030ULL;  // "ODC1B200"
 
 std::int64_t round256(std::int64_t x) { return (x + 255) / 256 * 256; }
@@ -100,6 +107,7 @@ struct odc_ctx {
     std::uint64_t mb_epoch = 0;  // completed minibatch_end calls
     std::uint64_t adams = 0;     // completed adam steps (published param epochs)
     std::vector<char> pushed;    // SLOT: unit touched in the current minibatch
+    bool grads_pending = false;  // RED: the grad shards hold a finished minibatch not yet consumed
     odc::AdamSeg* d_segs = nullptr;
     std::int64_t* d_seg_start = nullptr;
     std::int64_t adam_units = 0;
@@ -113,7 +121,7 @@ struct odc_ctx {
     char* at(int r, std::int64_t off) const { return peer[static_cast<std::size_t>(r)] + off; }
     unsigned long long* done_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kDoneOff)); }
     unsigned long long* epoch_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kEpochOff)); }
-    unsigned long long* acc_epoch_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kAccEpochOff)); }
+    unsigned long long* drain_of(int r) const { return reinterpret_cast<unsigned long long*>(at(r, kDrainOff)); }
     unsigned long long* err() const { return reinterpret_cast<unsigned long long*>(arena + kErrOff); }
     // element 0 of owner r's shard of unit u in each array
     unsigned short* param_of(int r, const Unit& u) const {
@@ -134,6 +142,26 @@ struct odc_ctx {
         if (!ready) throw StateError("odc context used before odc_ctx_ready()");
     }
     void dev() const { cuda_ok(cudaSetDevice(cfg.device), "cudaSetDevice"); }
+    bool red_mode() const { return cfg.push_mode == ODC_PUSH_RED; }
+    // RED: the caller is done with last minibatch's grad shards (this is the
+    // next ODC call after odc_minibatch_end without an AdamW step): zero them
+    // and let peers push again
+    void drain_pending(cudaStream_t s) {
+        if (!grads_pending) return;
+        std::vector<float*> ptrs;
+        std::vector<std::int64_t> cnt;
+        for (const Unit& u : units)
+            if (u.len(rank()) > 0) {
+                ptrs.push_back(f32_of(rank(), u.off_grad, u));
+                cnt.push_back(u.len(rank()));
+            }
+        if (!ptrs.empty())
+            cuda_ok(odc::launch_gated_zero(ptrs.data(), cnt.data(), static_cast<int>(ptrs.size()), nullptr, 0, 0, err(),
+                                           timeout_ns, s),
+                    "zero grad shards");
+        cuda_ok(odc::launch_publish(drain_of(rank()), mb_epoch, s), "publish drain epoch");
+        grads_pending = false;
+    }
     // rotation: rank r visits owners r+1, r+2, ..., r so that concurrent
     // fetches/pushes from all ranks spread over all owners' links
     int owner_at(int i) const { return (rank() + 1 + i) % world(); }
@@ -357,6 +385,7 @@ odc_status odc_set_params(odc_ctx_t ch, int layer, const float* src_full, void* 
         const Unit& u = c->unit(layer);
         c->dev();
         const int r = c->rank();
+        c->drain_pending(S(stream));
         cuda_ok(odc::launch_init_shard(c->f32_of(r, u.off_master, u), c->param_of(r, u), src_full + u.begin(r), u.len(r),
                                        S(stream)),
                 "set_params");
@@ -369,6 +398,7 @@ odc_status odc_fetch(odc_ctx_t ch, int layer, void* dst_full, void* stream) {
         c->need_ready();
         const Unit& u = c->unit(layer);
         c->dev();
+        c->drain_pending(S(stream));
         odc::SegTable t{};
         t.n = c->world();
         for (int i = 0; i < c->world(); ++i) {
@@ -415,12 +445,15 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
         if (grad_dtype != ODC_F32 && grad_dtype != ODC_BF16) throw ParamError("grad dtype must be ODC_F32 or ODC_BF16");
         const bool bf16 = grad_dtype == ODC_BF16;
         c->dev();
+        c->drain_pending(S(stream));
         if (c->slot_mode()) {
+            // the first push of a unit overwrites this client's slot: every owner
+            // must have finished its reduce of the previous minibatch
             const unsigned long long* gates[odc::kMaxSeg];
-            for (int r = 0; r < c->world(); ++r) gates[r] = c->epoch_of(r);
+            for (int r = 0; r < c->world(); ++r) gates[r] = c->drain_of(r);
             const bool first = !c->pushed[static_cast<std::size_t>(layer)];
             cuda_ok(odc::launch_slot_accumulate(reinterpret_cast<float*>(c->arena + u.off_slot), grad_full, bf16, u.elems,
-                                                weight, first, gates, first ? c->world() : 0, c->adams, c->err(),
+                                                weight, first, gates, first ? c->world() : 0, c->mb_epoch, c->err(),
                                                 c->timeout_ns, c->cfg.push_ctas, S(stream)),
                     "slot push");
             c->pushed[static_cast<std::size_t>(layer)] = 1;
@@ -434,7 +467,7 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
                 t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
                 t.dst[i] = c->acc_of(r, u);
                 t.elems[i] = u.len(r);
-                t.gate[i] = c->acc_epoch_of(r);
+                t.gate[i] = c->drain_of(r);
             }
             t.need = c->mb_epoch;  // the owner drained (converted + zeroed) the previous minibatch's sums
             t.err = c->err();
@@ -461,9 +494,9 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
                 t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
                 t.dst[i] = c->f32_of(r, u.off_grad, u);
                 t.elems[i] = u.len(r);
-                t.gate[i] = c->epoch_of(r);
+                t.gate[i] = c->drain_of(r);  // the owner consumed (zeroed) last minibatch's shard
             }
-            t.need = c->adams;
+            t.need = c->mb_epoch;
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
             cuda_ok(odc::launch_push_bulk(t, false, weight, 1.f, bf16, c->cfg.push_ctas, S(stream)), "push (bulk)");
@@ -476,9 +509,9 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
             t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
             t.dst[i] = c->f32_of(r, u.off_grad, u);
             t.elems[i] = u.len(r);
-            t.gate[i] = c->epoch_of(r);
+            t.gate[i] = c->drain_of(r);
         }
-        t.need = c->adams;
+        t.need = c->mb_epoch;
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
         cuda_ok(odc::launch_push_red(t, weight, bf16, c->cfg.push_ctas, S(stream)), "push");
@@ -499,14 +532,15 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
         if (offset < 0 || offset + n > u.len(target)) throw ProtocolError("payload does not fit the target shard");
         if (n == 0) return;
         c->dev();
+        c->drain_pending(S(stream));
         if (c->slot_mode()) {
             float* slot = reinterpret_cast<float*>(c->arena + u.off_slot);
             if (!c->pushed[static_cast<std::size_t>(layer)]) {
                 const unsigned long long* gates[odc::kMaxSeg];
-                for (int r = 0; r < c->world(); ++r) gates[r] = c->epoch_of(r);
+                for (int r = 0; r < c->world(); ++r) gates[r] = c->drain_of(r);
                 float* p = slot;
                 std::int64_t cnt = u.elems;
-                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, gates, c->world(), c->adams, c->err(), c->timeout_ns,
+                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, gates, c->world(), c->mb_epoch, c->err(), c->timeout_ns,
                                                S(stream)),
                         "slot zero");
                 c->pushed[static_cast<std::size_t>(layer)] = 1;
@@ -521,7 +555,7 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
             t.src[0] = payload;
             t.dst[0] = c->acc_of(target, u) + offset;
             t.elems[0] = n;
-            t.gate[0] = c->acc_epoch_of(target);
+            t.gate[0] = c->drain_of(target);
             t.need = c->mb_epoch;
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
@@ -533,8 +567,8 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
         t.src[0] = payload;
         t.dst[0] = c->f32_of(target, u.off_grad, u) + offset;
         t.elems[0] = n;
-        t.gate[0] = c->epoch_of(target);
-        t.need = c->adams;
+        t.gate[0] = c->drain_of(target);
+        t.need = c->mb_epoch;
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
         cuda_ok(odc::launch_push_red(t, weight, false, 8, S(stream)), "push_slice");
@@ -546,8 +580,9 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
         odc_ctx* c = C(ch);
         c->need_ready();
         c->dev();
+        c->drain_pending(S(stream));
         const unsigned long long* gates[odc::kMaxSeg];
-        for (int r = 0; r < c->world(); ++r) gates[r] = c->epoch_of(r);
+        for (int r = 0; r < c->world(); ++r) gates[r] = c->drain_of(r);
         if (c->slot_mode()) {
             // units this rank never pushed this minibatch still hold last
             // minibatch's sums: zero them once every owner finished reading
@@ -560,7 +595,7 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
                 }
             if (!ptrs.empty())
                 cuda_ok(odc::launch_gated_zero(ptrs.data(), cnt.data(), static_cast<int>(ptrs.size()), gates, c->world(),
-                                               c->adams, c->err(), c->timeout_ns, S(stream)),
+                                               c->mb_epoch, c->err(), c->timeout_ns, S(stream)),
                         "slot zero");
         }
         odc::BarrierArgs a{};
@@ -584,7 +619,10 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
                         "slot reduce");
             }
             std::fill(c->pushed.begin(), c->pushed.end(), 0);
+            // every client's slot of this minibatch is read: clients may overwrite them
+            cuda_ok(odc::launch_publish(c->drain_of(me), c->mb_epoch, S(stream)), "publish drain epoch");
         }
+        if (c->red_mode()) c->grads_pending = true;
         if (c->fixed_mode()) {  // every client's reductions landed before its done flag: convert + zero
             const int me = c->rank();
             const float inv = std::ldexp(1.0f, -c->cfg.fixed_frac_bits);
@@ -600,7 +638,7 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
                 }
             }
             cuda_ok(odc::launch_fixed_finalize(f, inv, S(stream)), "fixed finalize");
-            cuda_ok(odc::launch_publish(c->acc_epoch_of(me), c->mb_epoch, S(stream)), "publish acc epoch");
+            cuda_ok(odc::launch_publish(c->drain_of(me), c->mb_epoch, S(stream)), "publish drain epoch");
         }
     });
 }
@@ -652,9 +690,12 @@ odc_status odc_adam_step(odc_ctx_t ch, const odc_adam_cfg* cfg, void* stream) {
         const double bc2 = 1.0 - std::pow(static_cast<double>(cfg->beta2), cfg->step);
         a.step_size = static_cast<float>(cfg->lr / bc1);
         a.bc2_sqrt_inv = static_cast<float>(1.0 / std::sqrt(bc2));
-        cuda_ok(odc::launch_adam(a, c->adam_units, 0, S(stream)), "adam");
+        cuda_ok(odc::launch_adam(a, c->adam_units, 0, S(stream)), "adam");  // also zeroes the grad shards
         c->adams += 1;
-        cuda_ok(odc::launch_publish(c->epoch_of(c->rank()), c->adams, S(stream)), "publish epoch");
+        // new parameter epoch (fetch gate) and, RED, the consumed grad shards (push gate)
+        cuda_ok(odc::launch_publish(c->epoch_of(c->rank()), c->adams, S(stream), c->drain_of(c->rank()), c->mb_epoch),
+                "publish epoch");
+        c->grads_pending = false;
     });
 }
 
@@ -667,12 +708,29 @@ odc_status odc_ctx_check(odc_ctx_t ch, void* stream) {
         cuda_ok(cudaMemcpy(&e, c->err(), 8, cudaMemcpyDeviceToHost), "read err");
     });
     if (st != ODC_OK) return st;
-    if (e == odc::kErrTimeout) {
+    if (e & odc::kErrTimeout) {
         odc::set_last_error("device barrier watchdog fired: a peer never reached the minibatch barrier "
                             "or never published its parameter epoch");
         return ODC_ERR_TIMEOUT;
     }
+    if (e & odc::kErrFixedRange) {
+        odc::set_last_error("FIXED push out of range: a contribution |w*g| * 2^frac_bits reached 2^55 "
+                            "(int64 accumulator headroom) or was NaN/Inf; lower fixed_frac_bits");
+        return ODC_ERR_RANGE;
+    }
     return ODC_OK;
+}
+
+odc_status odc_ctx_flags(odc_ctx_t ch, uint64_t* flags, void* stream) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        if (!flags) throw ParamError("null flags");
+        c->dev();
+        cuda_ok(cudaStreamSynchronize(S(stream)), "sync");
+        unsigned long long e = 0;
+        cuda_ok(cudaMemcpy(&e, c->err(), 8, cudaMemcpyDeviceToHost), "read err");
+        *flags = e;
+    });
 }
 
 odc_status odc_copy_segments(int nseg, const void* const* srcs, void* const* dsts, const std::int64_t* bytes, int ctas,

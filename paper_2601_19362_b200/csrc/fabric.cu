@@ -95,6 +95,18 @@ struct odc_fabric {
 
     void set_device() const { cuda_ok(cudaSetDevice(device), "cudaSetDevice"); }
 
+    // one copy per simulated rank; the copy kernel's table holds kMaxSeg
+    // segments, so any rank count is split into tables of at most kMaxSeg
+    template <typename Fn>
+    void copy_ranks(Fn&& seg, int ctas, const char* what) {
+        for (int base = 0; base < ranks; base += odc::kMaxSeg) {
+            odc::SegTable t{};
+            t.n = std::min(odc::kMaxSeg, ranks - base);
+            for (int i = 0; i < t.n; ++i) seg(base + i, t.src[i], t.dst[i], t.bytes[i]);
+            cuda_ok(odc::launch_copy_segments(t, ctas, stream), what);
+        }
+    }
+
     template <typename T>
     void consume_t(int s, int c) {
         const std::size_t k = sidx(s, c);
@@ -163,14 +175,13 @@ struct odc_fabric {
     }
 
     void take_grads(void* host_out) {
-        odc::SegTable t{};
-        t.n = ranks;
-        for (int r = 0; r < ranks; ++r) {
-            t.src[r] = grads.ptr[r];
-            t.dst[r] = out + begin(r) * static_cast<std::int64_t>(es);
-            t.bytes[r] = len(r) * static_cast<std::int64_t>(es);
-        }
-        cuda_ok(odc::launch_copy_segments(t, 8, stream), "collect grads");
+        copy_ranks(
+            [&](int r, const char*& src, char*& dst, std::int64_t& bytes) {
+                src = grads.ptr[r];
+                dst = out + begin(r) * static_cast<std::int64_t>(es);
+                bytes = len(r) * static_cast<std::int64_t>(es);
+            },
+            8, "collect grads");
         cuda_ok(cudaMemcpyAsync(host_out, out, static_cast<std::size_t>(elems) * es, cudaMemcpyDeviceToHost, stream),
                 "D2H grads");
         cuda_ok(cudaMemsetAsync(grads.base, 0, static_cast<std::size_t>(stride_bytes * ranks), stream), "zero grads");
@@ -193,7 +204,7 @@ extern "C" {
 odc_status odc_fabric_create(int ranks, std::int64_t elems, odc_dtype dtype, int device, odc_fabric_t* out) {
     return odc::guard([&] {
         if (ranks < 1 || elems < 1) throw ParamError("need ranks >= 1 and elems >= 1");
-        if (ranks > odc::kMaxSeg * 64) throw ParamError("too many ranks");
+        if (ranks > 4096) throw ParamError("too many ranks");
         auto* f = new odc_fabric();
         try {
             f->ranks = ranks;
@@ -255,14 +266,14 @@ odc_status odc_fabric_set_params(odc_fabric_t fh, const char* id, const void* ho
         auto it = f->params.find(id);
         if (it == f->params.end()) it = f->params.emplace(id, f->alloc_set()).first;
         f->upload(host_full, n);
-        odc::SegTable t{};  // owners take their slices of the full vector
-        t.n = f->ranks;
-        for (int r = 0; r < f->ranks; ++r) {
-            t.src[r] = f->stage + f->begin(r) * static_cast<std::int64_t>(f->es);
-            t.dst[r] = it->second.ptr[r];
-            t.bytes[r] = f->len(r) * static_cast<std::int64_t>(f->es);
-        }
-        cuda_ok(odc::launch_copy_segments(t, 8, f->stream), "set_params");
+        const auto& dst = it->second.ptr;  // owners take their slices of the full vector
+        f->copy_ranks(
+            [&](int r, const char*& s, char*& d, std::int64_t& bytes) {
+                s = f->stage + f->begin(r) * static_cast<std::int64_t>(f->es);
+                d = dst[static_cast<std::size_t>(r)];
+                bytes = f->len(r) * static_cast<std::int64_t>(f->es);
+            },
+            8, "set_params");
         cuda_ok(cudaStreamSynchronize(f->stream), "sync");
     });
 }
@@ -274,14 +285,14 @@ odc_status odc_fabric_gather(odc_fabric_t fh, int client, const char* id, void* 
         auto it = f->params.find(id);
         if (it == f->params.end()) throw StateError(std::string("gather of uninitialized params '") + id + "'");
         f->set_device();
-        odc::SegTable t{};
-        t.n = f->ranks;
-        for (int r = 0; r < f->ranks; ++r) {
-            t.src[r] = it->second.ptr[r];
-            t.dst[r] = f->out + f->begin(r) * static_cast<std::int64_t>(f->es);
-            t.bytes[r] = f->len(r) * static_cast<std::int64_t>(f->es);
-        }
-        cuda_ok(odc::launch_copy_segments(t, 16, f->stream), "gather");
+        const auto& src = it->second.ptr;
+        f->copy_ranks(
+            [&](int r, const char*& s, char*& d, std::int64_t& bytes) {
+                s = src[static_cast<std::size_t>(r)];
+                d = f->out + f->begin(r) * static_cast<std::int64_t>(f->es);
+                bytes = f->len(r) * static_cast<std::int64_t>(f->es);
+            },
+            16, "gather");
         cuda_ok(cudaMemcpyAsync(host_out, f->out, static_cast<std::size_t>(f->elems) * f->es, cudaMemcpyDeviceToHost,
                                 f->stream),
                 "D2H gather");

@@ -56,7 +56,13 @@ struct FixFinal {
     std::int64_t elems[kMaxFinal];
 };
 
-enum : unsigned long long { kErrNone = 0, kErrTimeout = 1 };
+// device error word: a bit mask (sticky until the context is recreated)
+enum : unsigned long long {
+    kErrNone = 0,
+    kErrTimeout = 1,          // watchdog: a peer never reached a barrier / never published an epoch
+    kErrFixedRange = 2,       // FIXED push: a contribution saturated the int64 range or was NaN/Inf
+    kWarnFixedUnderflow = 4   // FIXED push: a nonzero contribution rounded to 0 (resolution, not an error)
+};
 
 std::uint64_t launches();
 void count_launch();
@@ -104,8 +110,10 @@ struct BarrierArgs {
     long long timeout_ns = 0;
 };
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
-// st.release.sys *flag = value (after everything earlier on the stream)
-cudaError_t launch_publish(unsigned long long* flag, unsigned long long value, cudaStream_t s);
+// st.release.sys *flag = value (after everything earlier on the stream);
+// optionally a second flag in the same launch
+cudaError_t launch_publish(unsigned long long* flag, unsigned long long value, cudaStream_t s,
+                           unsigned long long* flag2 = nullptr, unsigned long long value2 = 0);
 // wait for every gate >= need, then zero `n` floats at each of `ptrs`
 cudaError_t launch_gated_zero(float* const* ptrs, const std::int64_t* n, int count,
                               const unsigned long long* const* gates, int ngates, unsigned long long need,

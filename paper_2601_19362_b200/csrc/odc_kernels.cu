@@ -80,9 +80,9 @@ __device__ bool wait_geq(const unsigned long long* flag, unsigned long long need
     unsigned ns = 32;
     while (true) {
         if (ld_acquire_sys(flag) >= need) return true;
-        if (err && *reinterpret_cast<volatile unsigned long long*>(err) != kErrNone) return false;
+        if (err && (*reinterpret_cast<volatile unsigned long long*>(err) & kErrTimeout)) return false;
         if (global_ns() - t0 > timeout_ns) {
-            if (err) atomicExch(err, static_cast<unsigned long long>(kErrTimeout));
+            if (err) atomicOr(err, static_cast<unsigned long long>(kErrTimeout));
             return false;
         }
         __nanosleep(ns);
@@ -140,15 +140,18 @@ __global__ void __launch_bounds__(kCopyThreads) copy_segments_kernel(SegTable t)
     const std::int64_t total = first_chunk[t.n];
     int seg = 0;
     int gated_seg = -1;
+    bool seg_ok = true;  // gate result of gated_seg, kept for the segment's later chunks
     for (std::int64_t c = blockIdx.x; c < total; c += gridDim.x) {
         while (c >= first_chunk[seg + 1]) ++seg;
-        if (t.gate[seg] && gated_seg != seg) {  // on-demand readiness of this owner's shard
-            if (threadIdx.x == 0) gate_ok = wait_geq(t.gate[seg], t.need, t.err, t.timeout_ns);
-            __syncthreads();
-            const bool ok = gate_ok != 0;
-            __syncthreads();  // gate_ok may be rewritten at the next segment switch
-            gated_seg = seg;
-            if (!ok) continue;
+        if (t.gate[seg]) {  // on-demand readiness of this owner's shard
+            if (gated_seg != seg) {
+                if (threadIdx.x == 0) gate_ok = wait_geq(t.gate[seg], t.need, t.err, t.timeout_ns);
+                __syncthreads();
+                seg_ok = gate_ok != 0;
+                __syncthreads();  // gate_ok may be rewritten at the next segment switch
+                gated_seg = seg;
+            }
+            if (!seg_ok) continue;  // a timed-out owner's chunks are never copied
         }
         const SegPlan p = plans[seg];
         const char* src = t.src[seg];
@@ -466,6 +469,9 @@ __global__ void __launch_bounds__(kPushThreads) push_red_kernel(RedTable t, floa
                 red_sys_f32(t.dst[i] + tb + threadIdx.x, __fmul_rn(w, load_grad<BF16>(t.src[i], tb + threadIdx.x)));
         }
     }
+    // order this thread's remote reductions before anything later in the
+    // stream (the barrier kernel's release also covers them cumulatively)
+    __threadfence_system();
 }
 
 cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas, cudaStream_t s) {
@@ -603,8 +609,17 @@ cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc
 constexpr int kFixThreads = 256;
 
 
-__device__ __forceinline__ long long to_fixed(float w, float g, float scale) {
-    return __float2ll_rn(__fmul_rn(__fmul_rn(w, g), scale));
+// Range: a single contribution must satisfy |w*g*2^S| < 2^kFixedMaxLog2 (2^55),
+// leaving 8 guard bits so 256 maximal contributions cannot overflow the int64
+// sum. A contribution outside that range (or NaN/Inf) sets `range`; a nonzero
+// contribution that rounds to 0 sets `under` (resolution loss, not an error).
+constexpr float kFixedMax = 36028797018963968.0f;  // 2^55
+__device__ __forceinline__ long long to_fixed(float w, float g, float scale, bool& range, bool& under) {
+    const float x = __fmul_rn(__fmul_rn(w, g), scale);
+    if (!(fabsf(x) < kFixedMax)) range = true;
+    const long long q = __float2ll_rn(x);
+    if (q == 0 && x != 0.f) under = true;
+    return q;
 }
 __device__ __forceinline__ void red_sys_u64(long long* p, long long v) {
     asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -637,6 +652,7 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
     __shared__ std::int64_t head[kMaxSeg], lo[kMaxSeg], hi[kMaxSeg];
     __shared__ bool fast[kMaxSeg];
     __shared__ int gate_ok;
+    bool range = false, under = false;  // FIXED conversion flags of this thread
     if (threadIdx.x == 0) gate_ok = 1;
     __syncthreads();
     // FIXED: the owner drained its accumulator at its last minibatch end; F32: the owner's AdamW zeroed its grad shard
@@ -683,8 +699,8 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
                     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(buf + u));
                     if constexpr (FIXED) {
                         const float2 g = load_grad2<BF16>(t.src[i], e0 + E * u);
-                        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(to_fixed(w, g.x, scale)),
-                                     "l"(to_fixed(w, g.y, scale))
+                        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(to_fixed(w, g.x, scale, range, under)),
+                                     "l"(to_fixed(w, g.y, scale, range, under))
                                      : "memory");
                     } else {
                         const float4 g = load_grad4<BF16>(t.src[i], e0 + E * u);
@@ -719,7 +735,7 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
     }
     auto scalar = [&](int i, std::int64_t e) {
         const float g = load_grad<BF16>(t.src[i], e);
-        if constexpr (FIXED) red_sys_u64(static_cast<long long*>(t.dst[i]) + e, to_fixed(w, g, scale));
+        if constexpr (FIXED) red_sys_u64(static_cast<long long*>(t.dst[i]) + e, to_fixed(w, g, scale, range, under));
         else red_sys_f32(static_cast<float*>(t.dst[i]) + e, __fmul_rn(w, g));
     };
     for (int i = 0; i < t.n; ++i)  // segments whose src/dst alignment rules out the bulk path: scalar reductions
@@ -735,6 +751,11 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
             if (threadIdx.x < head[i]) scalar(i, threadIdx.x);
             if (body_end + threadIdx.x < n) scalar(i, body_end + threadIdx.x);
         }
+    }
+    if constexpr (FIXED) {  // sticky flags in the owner-independent local error word
+        const int any_range = __syncthreads_or(range), any_under = __syncthreads_or(under);
+        if (threadIdx.x == 0 && t.err && (any_range || any_under))
+            atomicOr(t.err, (any_range ? kErrFixedRange : 0ull) | (any_under ? kWarnFixedUnderflow : 0ull));
     }
 }
 
@@ -847,6 +868,12 @@ template cudaError_t launch_red_accumulate<float>(float*, const float*, std::int
 // ------------------------------------------------------------- barrier
 __global__ void barrier_kernel(BarrierArgs a) {
     const int t = threadIdx.x;
+    // Every push this rank issued earlier on the stream completed before this
+    // kernel started (kernel boundary); the sys-scope fence makes their
+    // effects (remote red/bulk reductions, slot stores) ordered before the
+    // flag stores below for every observer, independently of the cumulativity
+    // of the release.
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
     if (t < a.world) {
         // release: every push this rank issued earlier on the stream (kernel
         // boundaries order them before this thread) is visible to owner t
@@ -863,11 +890,17 @@ cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-__global__ void publish_kernel(unsigned long long* flag, unsigned long long v) { st_release_sys(flag, v); }
+__global__ void publish_kernel(unsigned long long* flag, unsigned long long v, unsigned long long* flag2,
+                               unsigned long long v2) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    st_release_sys(flag, v);
+    if (flag2) st_release_sys(flag2, v2);
+}
 
-cudaError_t launch_publish(unsigned long long* flag, unsigned long long value, cudaStream_t s) {
+cudaError_t launch_publish(unsigned long long* flag, unsigned long long value, cudaStream_t s,
+                           unsigned long long* flag2, unsigned long long value2) {
     count_launch();
-    publish_kernel<<<1, 1, 0, s>>>(flag, value);
+    publish_kernel<<<1, 1, 0, s>>>(flag, value, flag2, value2);
     return cudaGetLastError();
 }
 

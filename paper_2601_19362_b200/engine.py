@@ -145,8 +145,17 @@ class OdcEngine:
         return out
 
     def check(self, stream=None):
-        """Synchronise `stream` and raise BarrierTimeout if the watchdog fired."""
+        """Synchronise `stream`; raise BarrierTimeout if the watchdog fired,
+        RangeError if a FIXED-mode push saturated the fixed-point range."""
         check(lib().odc_ctx_check(self.h, _stream(stream)))
+
+    def flags(self, stream=None) -> int:
+        """Sticky device flags (synchronises `stream`): _lib.ODC_FLAG_TIMEOUT,
+        ODC_FLAG_FIXED_RANGE, ODC_FLAG_FIXED_UNDERFLOW (a nonzero w*g that the
+        FIXED push rounded to 0: resolution loss, not an error)."""
+        v = C.c_uint64(0)
+        check(lib().odc_ctx_flags(self.h, C.byref(v), _stream(stream)))
+        return int(v.value)
 
     @property
     def epoch(self) -> int:

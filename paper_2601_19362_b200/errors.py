@@ -41,8 +41,12 @@ class BarrierTimeout(DeviceError):  # ODC_ERR_TIMEOUT (no reference counterpart)
     code = 9
 
 
+class RangeError(DeviceError):  # ODC_ERR_RANGE: FIXED push saturation / non-finite (no reference counterpart)
+    code = 10
+
+
 _BY_CODE = {c.code: c for c in (ParamError, InfeasibleError, InvariantError, ProtocolError, StateError, ModeError,
-                                DeviceError, BarrierTimeout)}
+                                DeviceError, BarrierTimeout, RangeError)}
 
 
 def from_status(code: int, msg: str) -> OdcError:

@@ -32,6 +32,12 @@ class Shape:
         mlp = 3 * self.d * self.ffn
         return q + kv + o + mlp + 2 * self.d
 
+    def unit_sizes(self):
+        """FSDP units: 0 = embedding (+ final norm, + untied LM head), 1..L =
+        decoder layers (worker.unit_sizes computes the same from the layouts)."""
+        emb = self.vocab * self.d * (1 if self.tied else 2) + self.d
+        return [emb] + [self.layer_elems] * self.layers
+
     @property
     def nonembed_params(self) -> int:
         return self.layers * self.layer_elems + self.d  # + final norm

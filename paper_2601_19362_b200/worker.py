@@ -10,9 +10,10 @@ packed-varlen forward and a hand-written backward:
   minibatch end: comm.minibatch_end() then comm.adam()
 
 Dense layers are tcgen05 GEMMs (csrc/gemm.cu, operands used in place);
-attention is flash-attn varlen (library, sm_100 build); the elementwise
-glue (RMSNorm, bias+RoPE+split, SwiGLU, CE) is fused sm_100a kernels
-(csrc/worker_kernels.cu) and residual adds ride in the GEMM epilogue.
+attention is the tcgen05 causal varlen forward/backward (csrc/attention.cu,
+head_dim 128 only: any other shape raises, there is no library fallback);
+the elementwise glue (RMSNorm, bias+RoPE+split, SwiGLU, CE) is fused sm_100a
+kernels (csrc/worker_kernels.cu) and residual adds ride in the GEMM epilogue.
 Activations are kept for the backward by default (they fit 180 GB for the
 1.5B shape at 32K tokens). The 8B/14B shapes at 32K/64K tokens do not fit, so
 `recompute` keeps only each layer's input (+ the attention output and lse in
@@ -35,11 +36,6 @@ import torch
 from . import fused as F
 from . import gemm as G
 from .shapes import Shape
-
-try:  # library attention kernels (flash-attn 2.8, sm_100 cubins)
-    from flash_attn.flash_attn_interface import _flash_attn_varlen_backward, _flash_attn_varlen_forward
-except Exception:  # pragma: no cover - resolved at use
-    _flash_attn_varlen_forward = _flash_attn_varlen_backward = None
 
 ROPE_THETA = 1_000_000.0
 EPS = 1e-6
@@ -280,10 +276,11 @@ def attach_attn_items(b: Batch, seq_lens: Sequence[int], heads: int, device, kv_
 
 class Worker:
     def __init__(self, shape: Shape, comm, device, ce_chunk: int = 8192, max_positions: int = 65536,
-                 cache_params: bool = False, attn: str = "tcgen05", recompute: str = "none"):
-        if _flash_attn_varlen_forward is None:
-            raise ImportError("flash-attn (sm_100) is required for the worker's attention")
+                 cache_params: bool = False, recompute: str = "none"):
+        if shape.head_dim != 128:
+            raise ValueError(f"the tcgen05 attention kernels need head_dim 128, {shape.name} has {shape.head_dim}")
         self.s, self.comm, self.dev = shape, comm, torch.device(device)
+        self.max_positions = max_positions
         if recompute not in ("none", "selective", "full"):
             raise ValueError(f"recompute must be none|selective|full, got {recompute!r}")
         self.recompute = recompute
@@ -298,8 +295,6 @@ class Worker:
         self.egrad = torch.empty(self.sizes[0], dtype=torch.float32, device=self.dev)
         self.rope = F.rope_table(max_positions, shape.head_dim, ROPE_THETA, self.dev)
         self.tracer: Optional[Tracer] = None
-        # attention: own tcgen05 kernels (csrc/attention.cu) or flash-attn 2.8 (library) for both passes
-        self.attn = attn if shape.head_dim == 128 else "flash"
         # parameters cannot change inside a minibatch, so with
         # HBM to spare every unit is fetched once per minibatch and reused by
         # the backward and by later microbatches (ODC only: FSDP reshards)
@@ -348,11 +343,8 @@ class Worker:
         del qkv
         if o_lse is not None:
             o, lse = o_lse
-        elif self.attn == "tcgen05":
-            o, lse = F.attn_fwd(q, k, v, b.attn_items, 1.0 / math.sqrt(hd))
         else:
-            o, lse, _, _ = _flash_attn_varlen_forward(q, k, v, b.cu_seqlens, b.cu_seqlens, b.max_len, b.max_len,
-                                                      0.0, 1.0 / math.sqrt(hd), True)
+            o, lse = F.attn_fwd(q, k, v, b.attn_items, 1.0 / math.sqrt(hd))
         hm = G.linear_fwd(o.view(T, H * hd), P["o_w"], residual=x)
         bn, r2 = F.rmsnorm_fwd(hm, P["ln2"])
         gu = G.linear_fwd(bn, P["gu_w"])
@@ -384,7 +376,9 @@ class Worker:
         scale = 1.0 / math.sqrt(hd)
         lay = layer_layout(s)
         tab = self.rope
-        if self.attn == "tcgen05" and (b.attn_items is None or b.attn_bwd_items is None):
+        if b.max_len > self.max_positions:  # the RoPE table has max_positions rows (positions restart per sample)
+            raise ValueError(f"sample of {b.max_len} tokens exceeds the RoPE table ({self.max_positions} positions)")
+        if b.attn_items is None or b.attn_bwd_items is None:
             cu = b.cu_seqlens.tolist()
             attach_attn_items(b, [cu[i + 1] - cu[i] for i in range(len(cu) - 1)], H, self.dev, KV)
 
@@ -459,15 +453,7 @@ class Worker:
             # attention block
             do = G.linear_dgrad(dhm, P["o_w"])
             G.linear_wgrad(dhm, o.view(T, -1), out=Gv["o_w"])
-            if self.attn == "tcgen05":
-                dq, dk, dv = F.attn_bwd(q, k, v, o, do.view(T, H, hd), lse, b.attn_bwd_items, scale)
-            else:
-                dq = torch.empty_like(q)
-                dk = torch.empty_like(k)
-                dv = torch.empty_like(v)
-                _flash_attn_varlen_backward(do.view(T, H, hd), q, k, v, o, lse, dq, dk, dv, b.cu_seqlens,
-                                            b.cu_seqlens, b.max_len, b.max_len, 0.0, scale, True, -1, -1, 0.0, None,
-                                            False)
+            dq, dk, dv = F.attn_bwd(q, k, v, o, do.view(T, H, hd), lse, b.attn_bwd_items, scale)
             dqkv = F.qkv_rope_bwd(dq, dk, dv, tab, b.positions, H, KV, hd)
             del dq, dk, dv, do
             if "qkv_b" in Gv:

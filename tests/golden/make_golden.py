@@ -140,6 +140,37 @@ def main():
         sch.append({"ranks": N, "elems": M, "pushes": pushes, "seed": seed, "expected": out.tolist(), "peak": peak})
     dump("schedules.json", sch)
 
+    bench_plans()
+
+
+def bench_plans():
+    """The EXACT plans bench.py runs: the full 2,048-length workload (floored
+    at 512), minibatch 8 per rank, packing ratio 1 (budget = cap), at the
+    bench's cost model beta/alpha (paper_2601_19362_b200.shapes
+    beta_over_alpha_b200, 26,679.8 for Qwen2.5-1.5B) for every BASELINE model
+    and N = 1/2/4/8, both arms (LB-Mini for ODC, LB-Micro for FSDP). Stored as
+    the sha256 of the reference's solutions_to_json bytes plus the first step
+    in clear (the full dumps are ~0.1-0.3 MB each)."""
+    import hashlib
+
+    from paper_2601_19362_b200.shapes import SHAPES  # pure-Python constants (no product code runs)
+
+    out = []
+    for name, cap in (("qwen2.5-1.5b", 32768), ("llama-3-8b", 32768), ("qwen2.5-14b", 65536)):
+        beta = SHAPES[name].beta_over_alpha_b200()
+        _, lens = bench_workload(cap=cap)
+        for D in (1, 2, 4, 8):
+            for strat in ("lb-mini", "lb-micro"):
+                js = R.plan_json(strat, lens, D, 8, cap, 1.0, beta)
+                first = json.loads(js)["steps"][0]
+                out.append({"model": name, "cap": cap, "strategy": strat, "devices": D, "minibs": 8, "budget": cap,
+                            "alpha": 1.0, "beta": beta, "seed": 0, "sha256": hashlib.sha256(js.encode()).hexdigest(),
+                            "bytes": len(js), "steps": len(json.loads(js)["steps"]), "first_step": first})
+    dump("bench_plans.json", out)
+
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["bench_plans"]:
+        bench_plans()
+    else:
+        main()

@@ -179,3 +179,57 @@ def test_kernel_launch_counter_moves():
     eng.fetch(0, torch.empty(1024, dtype=torch.bfloat16, device=DEV))
     eng.check()
     assert _lib.kernel_launches() >= n0 + 2
+
+
+@pytest.mark.parametrize("mode", ["red", "slot", "fixed"])
+def test_two_minibatches_without_adam(mode):
+    """finalize_minibatch returns AND zeroes (inc/primitives.hpp:144-148): a
+    second minibatch with no AdamW in between must see only its own pushes
+    (RED: the owner drains its grad shard at its next ODC call; SLOT: the
+    first push of a unit reassigns the slot once the owner's reduce is done)."""
+    sizes = [1001, 65536 + 5]
+    eng = OdcEngine(sizes, push_mode=mode)
+    for l, n in enumerate(sizes):
+        eng.set_params(l, torch.zeros(n, device=DEV))
+    rng = np.random.default_rng(11)
+    for mb in range(3):
+        gs = [rng.integers(-8, 8, n).astype(np.float32) for n in sizes]  # exact in every mode
+        for l, g in enumerate(gs):
+            eng.push(l, torch.from_numpy(g).to(DEV), 0.5)
+        eng.minibatch_end()
+        for l, g in enumerate(gs):
+            got = eng.read_grad_shard(l).cpu().numpy()
+            assert np.array_equal(got, 0.5 * g), (mode, mb, l)
+        eng.check()
+    # a minibatch with no push at all returns zeros
+    eng.minibatch_end()
+    for l in range(len(sizes)):
+        assert not eng.read_grad_shard(l).cpu().numpy().any(), (mode, l)
+    eng.check()
+    eng.close()
+
+
+def test_fixed_push_range_error_and_underflow_flag():
+    """FIXED push: a contribution that saturates the int64 fixed-point range
+    (or is NaN) raises RangeError at the next check; a nonzero contribution
+    below the resolution only sets the underflow flag."""
+    eng = OdcEngine([4096], push_mode="fixed")
+    eng.set_params(0, torch.zeros(4096, device=DEV))
+    g = torch.full((4096,), 1e-20, device=DEV)  # < 2^-41: rounds to 0
+    eng.push(0, g, 1.0)
+    eng.minibatch_end()
+    assert eng.flags() == _lib.ODC_FLAG_FIXED_UNDERFLOW
+    eng.check()  # underflow is not an error
+    assert not eng.read_grad_shard(0).cpu().numpy().any()
+    eng.close()
+    for bad in (float(2 ** 16), float("nan")):  # 2^16 * 2^40 = 2^56 >= 2^55
+        eng = OdcEngine([4096], push_mode="fixed")
+        eng.set_params(0, torch.zeros(4096, device=DEV))
+        g = torch.zeros(4096, device=DEV)
+        g[1234] = bad
+        eng.push(0, g, 1.0)
+        eng.minibatch_end()
+        assert eng.flags() & _lib.ODC_FLAG_FIXED_RANGE
+        with pytest.raises(E.RangeError):
+            eng.check()
+        eng.close()

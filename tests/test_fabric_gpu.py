@@ -117,3 +117,22 @@ def test_random_interleavings_match_reference():
         got = np.concatenate(st.take_grads())
         assert got.tolist() == case["expected"] and peak == case["peak"]
         assert peak <= ((M + N - 1) // N) * N  # Appendix-B buffer bound
+
+
+@pytest.mark.parametrize("ranks", [17, 40])
+def test_fabric_more_ranks_than_one_copy_table(ranks):
+    """More simulated ranks than one copy-kernel table holds (16): set_params,
+    gather and finalize split their per-rank copies (verify-primitives
+    --clients 32 in the reference CLI)."""
+    elems = 1000 + ranks
+    rng = np.random.default_rng(ranks)
+    f, o = ShardFabric(ranks, elems, np.int64), O.ShardFabric(ranks, elems, np.int64)
+    p = rng.integers(-100, 100, elems)
+    f.set_params("w", p)
+    o.set_params("w", p)
+    assert np.array_equal(f.gather(3, "w"), o.gather(3, "w"))
+    for c in (0, ranks - 1, 5, 0):
+        g, w = rng.integers(-50, 50, elems), int(rng.integers(1, 4))
+        f.scatter_accumulate(c, g, w)
+        o.scatter_accumulate(c, g, w)
+    assert np.array_equal(np.concatenate(f.finalize_minibatch()), np.concatenate(o.finalize_minibatch()))

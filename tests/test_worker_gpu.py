@@ -1,5 +1,5 @@
 """Worker numerics: one packed-varlen microbatch through the hand-written
-forward/backward (tcgen05 GEMMs, flash-attn varlen, ODC fetch/push at world=1)
+forward/backward (tcgen05 GEMMs, tcgen05 attention, ODC fetch/push at world=1)
 vs a plain torch fp32 autograd model with the same weights and tokens.
 
 The worker computes in bf16 with fp32 accumulation, so the bar is a floating-
