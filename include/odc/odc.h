@@ -146,6 +146,11 @@ odc_status odc_ctx_destroy(odc_ctx_t ctx);
 /* IPC blob describing this rank's HBM arena (cudaIpcMemHandle + layout hash) */
 odc_status odc_ctx_export(odc_ctx_t ctx, void* blob, size_t cap, size_t* len);
 odc_status odc_ctx_import(odc_ctx_t ctx, int peer, const void* blob, size_t len);
+/* single-process mode: map peer `peer`'s arena from its context living in
+ * this process (same device: several ranks on one GPU, for protocol tests;
+ * another device: direct peer access over NVLink, enabled here). Same layout
+ * checks as odc_ctx_import. */
+odc_status odc_ctx_import_ctx(odc_ctx_t ctx, int peer, odc_ctx_t peer_ctx);
 /* after every peer was imported: builds the device pointer tables */
 odc_status odc_ctx_ready(odc_ctx_t ctx);
 /* bytes of HBM the arena holds on this rank */

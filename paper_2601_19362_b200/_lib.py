@@ -59,6 +59,7 @@ SIGNATURES = {
     "odc_ctx_destroy": (C.c_int, [vp]),
     "odc_ctx_export": (C.c_int, [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)]),
     "odc_ctx_import": (C.c_int, [vp, C.c_int, vp, C.c_size_t]),
+    "odc_ctx_import_ctx": (C.c_int, [vp, C.c_int, vp]),
     "odc_ctx_ready": (C.c_int, [vp]),
     "odc_ctx_arena_bytes": (C.c_int, [vp, i64p]),
     "odc_set_params": (C.c_int, [vp, C.c_int, vp, vp]),

@@ -102,6 +102,7 @@ struct odc_ctx {
     char* arena = nullptr;
     std::vector<char*> peer;  // peer[r] = r's arena mapped here (peer[rank] = arena)
     std::vector<bool> imported;
+    std::vector<bool> local_peer;  // mapped from a context of this process (odc_ctx_import_ctx): not an IPC mapping
     bool ready = false;
     long long timeout_ns = 60LL * 1000 * 1000 * 1000;
     std::uint64_t mb_epoch = 0;  // completed minibatch_end calls
@@ -280,6 +281,7 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
             cuda_ok(cudaDeviceSynchronize(), "memset arena sync");
             c->peer.assign(static_cast<std::size_t>(cfg->world), nullptr);
             c->imported.assign(static_cast<std::size_t>(cfg->world), false);
+            c->local_peer.assign(static_cast<std::size_t>(cfg->world), false);
             c->peer[static_cast<std::size_t>(cfg->rank)] = c->arena;
             c->imported[static_cast<std::size_t>(cfg->rank)] = true;
             c->pushed.assign(c->units.size(), 0);
@@ -296,7 +298,9 @@ odc_status odc_ctx_destroy(odc_ctx_t c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     for (int r = 0; r < static_cast<int>(c->peer.size()); ++r)
-        if (r != c->cfg.rank && c->peer[static_cast<std::size_t>(r)]) cudaIpcCloseMemHandle(c->peer[static_cast<std::size_t>(r)]);
+        if (r != c->cfg.rank && c->peer[static_cast<std::size_t>(r)] &&
+            !(r < static_cast<int>(c->local_peer.size()) && c->local_peer[static_cast<std::size_t>(r)]))
+            cudaIpcCloseMemHandle(c->peer[static_cast<std::size_t>(r)]);
     if (c->arena) cudaFree(c->arena);
     if (c->d_segs) cudaFree(c->d_segs);
     if (c->d_seg_start) cudaFree(c->d_seg_start);
@@ -338,6 +342,30 @@ odc_status odc_ctx_import(odc_ctx_t ch, int peer, const void* blob, std::size_t 
         cuda_ok(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
         c->peer[static_cast<std::size_t>(peer)] = static_cast<char*>(p);
         c->imported[static_cast<std::size_t>(peer)] = true;
+    });
+}
+
+odc_status odc_ctx_import_ctx(odc_ctx_t ch, int peer, odc_ctx_t peer_ctx) {
+    return odc::guard([&] {
+        odc_ctx* c = C(ch);
+        odc_ctx* p = C(peer_ctx);
+        if (peer < 0 || peer >= c->world()) throw ParamError("peer out of range");
+        if (peer == c->rank()) return;
+        if (p->rank() != peer || p->world() != c->world()) throw ParamError("context does not belong to this peer/world");
+        if (p->layout_hash != c->layout_hash || p->arena_bytes != c->arena_bytes)
+            throw ParamError("peer arena layout differs (different layer sizes or push mode)");
+        c->dev();
+        if (p->cfg.device != c->cfg.device) {  // another GPU of this process: direct peer access over NVLink
+            int ok = 0;
+            cuda_ok(cudaDeviceCanAccessPeer(&ok, c->cfg.device, p->cfg.device), "cudaDeviceCanAccessPeer");
+            if (!ok) throw ParamError("no peer access between the two devices");
+            const cudaError_t e = cudaDeviceEnablePeerAccess(p->cfg.device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else cuda_ok(e, "cudaDeviceEnablePeerAccess");
+        }
+        c->peer[static_cast<std::size_t>(peer)] = p->arena;
+        c->imported[static_cast<std::size_t>(peer)] = true;
+        c->local_peer[static_cast<std::size_t>(peer)] = true;
     });
 }
 

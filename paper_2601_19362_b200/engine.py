@@ -46,7 +46,7 @@ def _ptr(t: torch.Tensor):
 class OdcEngine:
     def __init__(self, layer_elems: Sequence[int], rank: int = 0, world: int = 1, device: Optional[int] = None,
                  push_mode: str = "red", fetch_ctas: int = 0, push_ctas: int = 0, timeout_s: float = 60.0,
-                 group=None, fetch_engine: str = "tma", fixed_frac_bits: int = 0):
+                 group=None, fetch_engine: str = "tma", fixed_frac_bits: int = 0, _defer_ready: bool = False):
         self.layer_elems = [int(x) for x in layer_elems]
         self.rank, self.world = rank, world
         if device is None:
@@ -60,10 +60,30 @@ class OdcEngine:
         h = C.c_void_p()
         check(lib().odc_ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h
+        self.adam_steps = 0
+        if _defer_ready:  # local_group wires the peers itself
+            return
         if world > 1:
             self._exchange(group)
         check(lib().odc_ctx_ready(self.h))
-        self.adam_steps = 0
+
+    @classmethod
+    def local_group(cls, layer_elems: Sequence[int], world: int, devices: Sequence[int], **kw):
+        """Single-process mode: `world` ranks in THIS process, rank r on
+        devices[r % len(devices)], every peer arena mapped directly
+        (odc_ctx_import_ctx) — several ranks per GPU for protocol tests on a
+        one-GPU box, or one process driving several GPUs over NVLink. The
+        ranks' operations are stream-ordered per rank; the device-side flag
+        protocol is the same as across processes."""
+        engs = [cls(layer_elems, rank=r, world=world, device=devices[r % len(devices)], _defer_ready=True, **kw)
+                for r in range(world)]
+        for e in engs:
+            for p in engs:
+                if p.rank != e.rank:
+                    check(lib().odc_ctx_import_ctx(e.h, p.rank, p.h))
+        for e in engs:
+            check(lib().odc_ctx_ready(e.h))
+        return engs
 
     def _exchange(self, group):
         from .dist import exchange_blobs

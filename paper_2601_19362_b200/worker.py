@@ -224,6 +224,29 @@ def chrome_trace(events_per_rank) -> dict:
     return {"traceEvents": evs, "displayTimeUnit": "ms"}
 
 
+def trace_busy_total(trace: dict, world: int):
+    """Per-rank busy time and step span from a measured trace: busy = summed
+    durations of the rank's compute spans ("fwd"/"bwd": the reference's
+    per_device_busy, src/commsim.cpp:119-121 — the "barrier" span is the wait
+    at the minibatch end, i.e. idle), total = the span from the earliest event
+    start to the latest event end over all ranks (us)."""
+    evs = trace["traceEvents"]
+    busy = [0.0] * world
+    for e in evs:
+        if e["cat"] == "compute" and not e["name"].startswith("barrier"):
+            busy[e["pid"]] += e["dur"]
+    t0 = min(e["ts"] for e in evs)
+    t1 = max(e["ts"] + e["dur"] for e in evs)
+    return busy, t1 - t0
+
+
+def trace_idle_fraction(trace: dict, world: int) -> float:
+    """The reference's bubble rate (src/runtime.cpp:43, src/commsim.cpp:232),
+    1 - sum(busy) / (D * T), applied to a measured trace."""
+    busy, total = trace_busy_total(trace, world)
+    return 1.0 - sum(busy) / (world * total)
+
+
 # --------------------------------------------------------------- worker
 @dataclass
 class Batch:

@@ -93,7 +93,7 @@ def _r(*s, scale=0.5):
                                           ("down", 8960, 1536)])
 def test_layer_gemms_at_32k_tokens(name, inn, out):
     T = 32768
-    torch.manual_seed(hash(name) % 1000)
+    torch.manual_seed(len(name) * 7 + inn)
     x, w, dy = _r(T, inn), _r(out, inn, scale=0.02), _r(T, out)
     y = G.linear_fwd(x, w)
     assert rel_l2(y, x.float() @ w.float().t()) < 1e-2

@@ -145,3 +145,51 @@ def test_recompute_matches_stored_activations():
     for g in grads[1:]:
         for a, b in zip(grads[0], g):
             torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-7)
+
+
+def test_trace_schema_and_idle_fraction():
+    """the measured timeline uses the reference's Chrome-trace
+    schema (src/commsim.cpp:240-258) and feeds the reference's bubble formula
+    (src/runtime.cpp:43); the result equals the oracle's bubble_rate on the
+    same per-rank busy times, and the compute spans cover the step."""
+    import re
+
+    from oracle import odc_oracle as O
+
+    s = TINY
+    sizes = W.unit_sizes(s)
+    gen = torch.Generator(device=DEV).manual_seed(5)
+    eng = OdcEngine(sizes, push_mode="red")
+    for u in range(len(sizes)):
+        eng.set_params(u, W.init_unit(s, u, gen, DEV))
+    wk = W.Worker(s, W.OdcComm(eng), DEV, ce_chunk=128)
+    wk.tracer = W.Tracer(0)
+    cur = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    wk.tracer.start(cur)
+    lens = [37, 100, 63, 200]
+    for mb in ([0, 1], [2, 3]):
+        wk.microbatch(W.make_batch(lens, mb, s.vocab, DEV), 0.5)
+    row = wk.tracer.span("barrier", 0, cur, False)
+    wk.minibatch_end()
+    W.Tracer.end(row, cur)
+    torch.cuda.synchronize()
+    tr = W.chrome_trace([wk.tracer.events()])
+    assert tr["displayTimeUnit"] == "ms" and tr["traceEvents"]
+    kinds = set()
+    for e in tr["traceEvents"]:
+        assert set(e) <= {"name", "cat", "ph", "pid", "tid", "ts", "dur", "args"}
+        m = re.fullmatch(r"(\w+) m(\d+) l(\d+)", e["name"])
+        assert m, e["name"]
+        kinds.add(m.group(1))
+        assert e["ph"] == "X" and e["pid"] == 0 and e["dur"] >= 0 and e["ts"] >= 0
+        assert e["cat"] == ("comm" if m.group(1) in ("gather", "reduce") else "compute")
+        assert e["tid"] == (1 if e["cat"] == "comm" else 0)
+        if e["cat"] == "comm":
+            assert e["args"]["volume_elems"] > 0
+    assert kinds == {"gather", "reduce", "fwd", "bwd", "barrier"}
+    busy, total = W.trace_busy_total(tr, 1)
+    idle = W.trace_idle_fraction(tr, 1)
+    assert idle == pytest.approx(O.bubble_rate(busy, total), abs=1e-12)
+    assert 0.0 <= idle < 1.0
+    eng.check()
