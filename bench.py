@@ -860,7 +860,7 @@ def main():
     push_bytes = M * 12 if world == 1 else (world - 1) * ((M + world - 1) // world) * P4_BYTES_F32
     big = (M + world - 1) // world >= (1 << 20)  # engine.cu: bulk reductions from 1M-element shards
     push_kernel = {"red": "push_bulk_kernel<F32>" if big else "push_red_kernel", "fixed": "push_bulk_kernel<FIXED>",
-                   "slot": "slot_accumulate_kernel"}[args.push_mode]
+                   "slot": "push_bulk_kernel<F32> (slot store/add at the owner)"}[args.push_mode]
     push_info = {"kernel": push_kernel,
                  "ms_per_launch": round(p_ms, 4), "GBps": round(push_bytes / (p_ms / 1e3) / 1e9, 1)}
 

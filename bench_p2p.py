@@ -11,6 +11,16 @@ S = bytes of one rank's bf16 parameter shard. Per rank and op:
   reduce_scatter torch.distributed.reduce_scatter_tensor, same fp32 bytes
   push_fixed     (--variants fixed:CTAS) deterministic int64 fixed-point push;
                  GB/s counts its int64 wire bytes ((N-1)*4S)
+  fetch_ce       the fetch through the copy engines (cudaMemcpyAsync peer ->
+                 local per owner, after the device gate): the driver's
+                 cudaMemcpyPeerAsync path
+  push_slot      SLOT-mode push as it runs in a step: the unit's first push of
+                 the minibatch STORES w*g into this client's slot at every
+                 owner (timed alone; the untimed minibatch_end between reps
+                 releases the slots), fp32 wire bytes ((N-1)*2S)
+  --sync         the paper's synchronous-launch protocol: every op
+                 alone between barriers (torch barrier + device sync before
+                 and after), time = max over ranks per op, averaged
 GB/s = algorithmic NVLink bytes per rank ((N-1)*S for bf16 gathers,
 (N-1)*2S for fp32 reductions) / op time, op time = max over ranks of the
 CUDA-event time of R back-to-back ops divided by R (barrier + sync around).
@@ -41,6 +51,7 @@ def main():
     ap.add_argument("--push-ctas", type=int, default=0)
     ap.add_argument("--fetch-engine", default="tma", choices=["tma", "ldg", "ce"])
     ap.add_argument("--variants", default="", help="extra fetch variants engine:ctas,... and push:ctas,...")
+    ap.add_argument("--sync", action="store_true", help="synchronous-launch protocol (barrier around every op)")
     args = ap.parse_args()
 
     import torch
@@ -57,7 +68,27 @@ def main():
     stream = torch.cuda.current_stream()
     rows = []
 
-    def timed(fn, reps):
+    def timed_sync(fn, reps, after=None):
+        tot = 0.0
+        for _ in range(reps + 1):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if after is not None:
+                after()
+            if _ > 0:  # the first op is a warm-up
+                tot += t.item()
+        return tot / reps
+
+    def timed(fn, reps, after=None):
+        if args.sync or after is not None:
+            return timed_sync(fn, reps, after)
         fn()
         torch.cuda.synchronize()
         dist.barrier()
@@ -85,13 +116,20 @@ def main():
         mine = torch.empty(shard, dtype=torch.bfloat16, device=dev)
         red_out = torch.empty(shard, dtype=torch.float32, device=dev)
         reps = max(3, min(args.reps, int(args.reps * (16 << 20) / max(S, 1 << 20))))
+        ce = OdcEngine([M], rank=rank, world=world, device=local, fetch_engine="ce")
+        ce.set_params(0, torch.zeros(M, device=dev))
+        sl = OdcEngine([M], rank=rank, world=world, device=local, push_mode="slot", push_ctas=args.push_ctas)
+        sl.set_params(0, torch.zeros(M, device=dev))
+        torch.cuda.synchronize()
+        dist.barrier()
         ops = {
             "odc_fetch": (lambda: eng.fetch(0, full), (world - 1) * S),
+            "odc_fetch_ce": (lambda: ce.fetch(0, full), (world - 1) * S),
             "odc_push": (lambda: eng.push(0, grad, 1.0), (world - 1) * 2 * S),
             "nccl_all_gather": (lambda: dist.all_gather_into_tensor(full, mine), (world - 1) * S),
             "nccl_reduce_scatter": (lambda: dist.reduce_scatter_tensor(red_out, grad), (world - 1) * 2 * S),
         }
-        extra = []
+        extra = [ce, sl]
         for v in [x for x in args.variants.split(",") if x]:
             kind, ctas = v.split(":")
             if kind == "push":
@@ -107,8 +145,10 @@ def main():
             extra.append(e2)
         torch.cuda.synchronize()
         dist.barrier()
-        for name, (fn, nbytes) in ops.items():
-            ms = timed(fn, reps)
+        ops["odc_push_slot"] = ((lambda: sl.push(0, grad, 1.0)), (world - 1) * 2 * S, lambda: sl.minibatch_end())
+        for name, op in ops.items():
+            fn, nbytes = op[0], op[1]
+            ms = timed(fn, reps, op[2] if len(op) > 2 else None)
             row = {"op": name, "world": world, "shard_bytes": S, "ms": round(ms, 5),
                    "GBps": round(nbytes / (ms / 1e3) / 1e9, 1)}
             rows.append(row)
@@ -124,10 +164,11 @@ def main():
     if rank == 0:
         os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
         sizes = sorted({r["shard_bytes"] for r in rows})
-        names = ["odc_fetch", "nccl_all_gather", "odc_push", "nccl_reduce_scatter"]
+        names = ["odc_fetch", "odc_fetch_ce", "nccl_all_gather", "odc_push", "odc_push_slot", "nccl_reduce_scatter"]
         names += sorted({r["op"] for r in rows} - set(names))
         with open(args.out, "w") as f:
-            f.write(f"# P2P fetch/push vs NCCL, N={world} (GB/s of algorithmic NVLink bytes per rank)\n\n")
+            f.write(f"# P2P fetch/push vs NCCL, N={world} (GB/s of algorithmic NVLink bytes per rank)"
+                    f"{' — synchronous launch (barrier around every op)' if args.sync else ''}\n\n")
             f.write("| shard S | " + " | ".join(names) + " |\n|---|" + "---|" * len(names) + "\n")
             for S in sizes:
                 cells = []

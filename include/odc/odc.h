@@ -54,8 +54,13 @@ typedef enum {
     /* remote red.global.add.v4.f32 straight into the owner's fp32 gradient
      * shard over NVLink; order across clients is not fixed */
     ODC_PUSH_RED = 0,
-    /* deterministic: per-source slot (single writer, push order), reduced by
-     * the owner at the minibatch barrier in fixed rank order 0..N-1 */
+    /* deterministic: every client owns one slot per unit AT EACH OWNER
+     * (capacity = block, the reference's per-(server, client) slot,
+     * inc/primitives.hpp:99-136); a push stores w*g into it over NVLink (the
+     * unit's first push of the minibatch) or adds it (later pushes: single
+     * writer, stream order); at the minibatch barrier the owner sums the
+     * slots of the clients that pushed, in fixed rank order 0..N-1 (local
+     * HBM). Memory: N * block per unit per rank. */
     ODC_PUSH_SLOT = 1,
     /* deterministic in bounded memory: each pushed w*g is rounded once to an
      * int64 fixed-point value (2^-fixed_frac_bits resolution) and added into
@@ -224,6 +229,14 @@ odc_status odc_l2_flush(void* scratch, int64_t bytes, void* stream);
 odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, int64_t M, int64_t N, int64_t K,
                          int64_t lda, int64_t ldb, int64_t ldd, int a_mn_major, int b_mn_major, int d_dtype,
                          int accumulate, void* stream);
+
+/* gate/up projection with SwiGLU fused into the epilogue (2-CTA tcgen05 GEMM):
+ * gu [T][2*ffn] = X [T][d] · W^T with W = [gate; up] [2*ffn][d] (as odc_gemm_bf16),
+ * and m [T][ffn] = silu(gate) * up computed from the bf16-rounded gu values
+ * (bit-identical to odc_w_swiglu_fwd). Output tile n pairs gate rows
+ * [128n, 128n+128) with up rows ffn + [128n, 128n+128). ffn % 128 == 0. */
+odc_status odc_gemm_gate_up_swiglu(const void* X, const void* W, void* gu, void* m, int64_t T, int64_t ffn, int64_t d,
+                                   void* stream);
 
 /* Causal varlen flash-attention forward on tcgen05 (head_dim 128, GQA).
  * q [T][H][128], k/v [T][KV][128] bf16; out [T][H][128]; lse [H][T] fp32 (natural log).

@@ -11,7 +11,8 @@
 //     grad   f32  [block+4]  stored at pad = begin % 4    caller's full-layer
 //     master f32  [block+4]                               buffers, so fetch
 //     m, v   f32  [block+4]                               and push run the
-//     slot   f32  [M_l]      (SLOT push mode only)        16-byte vector path)
+//     slot   f32  [N][block+4] (SLOT push mode only)      16-byte vector path)
+//                            owner-side slot of every client, same padding
 //     acc    i64  [block+2]  (FIXED push mode only) stored at pad = begin % 2
 //
 // Mapping onto the reference (inc/ = /root/reference/proj/include/odcsim/):
@@ -80,6 +81,7 @@ std::int64_t round256(std::int64_t x) { return (x + 255) / 256 * 256; }
 struct Unit {
     std::int64_t elems = 0, block = 0;
     std::int64_t off_param = 0, off_grad = 0, off_master = 0, off_m = 0, off_v = 0, off_slot = -1, off_acc = -1;
+    std::int64_t slot_stride = 0;  // bytes between two clients' slots (SLOT mode)
     std::int64_t begin(int r) const { return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r) * block); }
     std::int64_t len(int r) const { return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r + 1) * block) - begin(r); }
 };
@@ -107,7 +109,8 @@ struct odc_ctx {
     long long timeout_ns = 60LL * 1000 * 1000 * 1000;
     std::uint64_t mb_epoch = 0;  // completed minibatch_end calls
     std::uint64_t adams = 0;     // completed adam steps (published param epochs)
-    std::vector<char> pushed;    // SLOT: unit touched in the current minibatch
+    std::vector<char> touched;   // SLOT: [unit][owner] this client wrote its slot at the owner this minibatch
+    std::int64_t off_marks = -1;  // SLOT: [unit][client] u64 "pushed in minibatch" marks (owner side)
     bool grads_pending = false;  // RED: the grad shards hold a finished minibatch not yet consumed
     odc::AdamSeg* d_segs = nullptr;
     std::int64_t* d_seg_start = nullptr;
@@ -130,6 +133,16 @@ struct odc_ctx {
     }
     float* f32_of(int r, std::int64_t off, const Unit& u) const {
         return reinterpret_cast<float*>(at(r, off)) + u.begin(r) % 4;
+    }
+    // SLOT mode: client c's slot at owner r (co-aligned like the grad shard) and its mark
+    float* slot_of(int r, const Unit& u, int client) const {
+        return reinterpret_cast<float*>(at(r, u.off_slot + client * u.slot_stride)) + u.begin(r) % 4;
+    }
+    unsigned long long* mark_of(int r, int layer, int client) const {
+        return reinterpret_cast<unsigned long long*>(at(r, off_marks)) + static_cast<std::int64_t>(layer) * world() + client;
+    }
+    char& touched_at(int layer, int owner) {
+        return touched[static_cast<std::size_t>(layer) * static_cast<std::size_t>(world()) + static_cast<std::size_t>(owner)];
     }
     // FIXED mode int64 accumulator: element parity == global index parity
     long long* acc_of(int r, const Unit& u) const {
@@ -262,13 +275,18 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
                 off += f32;
                 if (cfg->push_mode == ODC_PUSH_SLOT) {
                     u.off_slot = off;
-                    off += round256(u.elems * 4);
+                    u.slot_stride = f32;
+                    off += f32 * cfg->world;
                 }
                 if (cfg->push_mode == ODC_PUSH_FIXED) {
                     u.off_acc = off;
                     off += round256((u.block + 2) * 8);
                 }
                 c->units.push_back(u);
+            }
+            if (cfg->push_mode == ODC_PUSH_SLOT) {
+                c->off_marks = off;
+                off += round256(static_cast<std::int64_t>(cfg->n_layers) * cfg->world * 8);
             }
             c->arena_bytes = off;
             c->layout_hash = h;
@@ -284,7 +302,7 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
             c->local_peer.assign(static_cast<std::size_t>(cfg->world), false);
             c->peer[static_cast<std::size_t>(cfg->rank)] = c->arena;
             c->imported[static_cast<std::size_t>(cfg->rank)] = true;
-            c->pushed.assign(c->units.size(), 0);
+            c->touched.assign(c->units.size() * static_cast<std::size_t>(cfg->world), 0);
         } catch (...) {
             odc_ctx_destroy(c);
             throw;
@@ -475,16 +493,28 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
         c->dev();
         c->drain_pending(S(stream));
         if (c->slot_mode()) {
-            // the first push of a unit overwrites this client's slot: every owner
-            // must have finished its reduce of the previous minibatch
-            const unsigned long long* gates[odc::kMaxSeg];
-            for (int r = 0; r < c->world(); ++r) gates[r] = c->drain_of(r);
-            const bool first = !c->pushed[static_cast<std::size_t>(layer)];
-            cuda_ok(odc::launch_slot_accumulate(reinterpret_cast<float*>(c->arena + u.off_slot), grad_full, bf16, u.elems,
-                                                weight, first, gates, first ? c->world() : 0, c->mb_epoch, c->err(),
-                                                c->timeout_ns, c->cfg.push_ctas, S(stream)),
-                    "slot push");
-            c->pushed[static_cast<std::size_t>(layer)] = 1;
+            // w*g for every owner goes straight into this client's slot AT THE OWNER over NVLink:
+            // stored by the unit's first push of the minibatch (after the owner's reduce of the
+            // previous minibatch released the slot), added (single writer, stream order) by later ones
+            odc::BulkTable t{};
+            t.n = c->world();
+            const int me = c->rank();
+            for (int i = 0; i < c->world(); ++i) {
+                const int r = c->owner_at(i);
+                t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
+                t.dst[i] = c->slot_of(r, u, me);
+                t.elems[i] = u.len(r);
+                t.gate[i] = c->drain_of(r);
+                const bool first = !c->touched_at(layer, r);
+                t.assign[i] = first;
+                t.mark[i] = first ? c->mark_of(r, layer, me) : nullptr;
+                c->touched_at(layer, r) = 1;
+            }
+            t.mark_value = c->mb_epoch + 1;
+            t.need = c->mb_epoch;
+            t.err = c->err();
+            t.timeout_ns = c->timeout_ns;
+            cuda_ok(odc::launch_push_bulk(t, false, weight, 1.f, bf16, c->cfg.push_ctas, S(stream)), "push (slot)");
             return;
         }
         if (c->fixed_mode()) {
@@ -562,19 +592,27 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
         c->dev();
         c->drain_pending(S(stream));
         if (c->slot_mode()) {
-            float* slot = reinterpret_cast<float*>(c->arena + u.off_slot);
-            if (!c->pushed[static_cast<std::size_t>(layer)]) {
-                const unsigned long long* gates[odc::kMaxSeg];
-                for (int r = 0; r < c->world(); ++r) gates[r] = c->drain_of(r);
+            const int me = c->rank();
+            float* slot = c->slot_of(target, u, me);
+            const bool first = !c->touched_at(layer, target);
+            if (first) {  // the slot still holds an older minibatch: zero it once the owner released it
                 float* p = slot;
-                std::int64_t cnt = u.elems;
-                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, gates, c->world(), c->mb_epoch, c->err(), c->timeout_ns,
-                                               S(stream)),
+                std::int64_t cnt = u.len(target);
+                const unsigned long long* gate = c->drain_of(target);
+                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, &gate, 1, c->mb_epoch, c->err(), c->timeout_ns, S(stream)),
                         "slot zero");
-                c->pushed[static_cast<std::size_t>(layer)] = 1;
+                c->touched_at(layer, target) = 1;
             }
-            cuda_ok(odc::launch_accumulate<float>(slot + u.begin(target) + offset, payload, n, weight, S(stream)),
-                    "slot slice");
+            odc::BulkTable t{};
+            t.n = 1;
+            t.src[0] = payload;
+            t.dst[0] = slot + offset;
+            t.elems[0] = n;
+            t.mark[0] = first ? c->mark_of(target, layer, me) : nullptr;
+            t.mark_value = c->mb_epoch + 1;
+            t.err = c->err();
+            t.timeout_ns = c->timeout_ns;
+            cuda_ok(odc::launch_push_bulk(t, false, weight, 1.f, false, 8, S(stream)), "push_slice (slot)");
             return;
         }
         if (c->fixed_mode()) {
@@ -609,23 +647,6 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
         c->need_ready();
         c->dev();
         c->drain_pending(S(stream));
-        const unsigned long long* gates[odc::kMaxSeg];
-        for (int r = 0; r < c->world(); ++r) gates[r] = c->drain_of(r);
-        if (c->slot_mode()) {
-            // units this rank never pushed this minibatch still hold last
-            // minibatch's sums: zero them once every owner finished reading
-            std::vector<float*> ptrs;
-            std::vector<std::int64_t> cnt;
-            for (std::size_t l = 0; l < c->units.size(); ++l)
-                if (!c->pushed[l]) {
-                    ptrs.push_back(reinterpret_cast<float*>(c->arena + c->units[l].off_slot));
-                    cnt.push_back(c->units[l].elems);
-                }
-            if (!ptrs.empty())
-                cuda_ok(odc::launch_gated_zero(ptrs.data(), cnt.data(), static_cast<int>(ptrs.size()), gates, c->world(),
-                                               c->mb_epoch, c->err(), c->timeout_ns, S(stream)),
-                        "slot zero");
-        }
         odc::BarrierArgs a{};
         a.world = c->world();
         a.rank = c->rank();
@@ -636,18 +657,26 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
         a.timeout_ns = c->timeout_ns;
         cuda_ok(odc::launch_barrier(a, S(stream)), "barrier");
         c->mb_epoch += 1;
-        if (c->slot_mode()) {
+        if (c->slot_mode()) {  // every client's slot writes landed before its done flag: rank-order reduce
             const int me = c->rank();
-            for (const Unit& u : c->units) {
-                const float* srcs[odc::kMaxSeg];
-                for (int s = 0; s < c->world(); ++s)  // fixed rank order 0..N-1
-                    srcs[s] = reinterpret_cast<const float*>(c->at(s, u.off_slot)) + u.begin(me);
-                cuda_ok(odc::launch_reduce_sources(c->f32_of(me, u.off_grad, u), srcs, c->world(), u.len(me),
-                                                   c->cfg.push_ctas > 0 ? c->cfg.push_ctas : 0, S(stream)),
-                        "slot reduce");
+            odc::SlotReduce r{};
+            r.nsrc = c->world();
+            r.epoch = c->mb_epoch;
+            for (std::size_t l = 0; l < c->units.size(); ++l) {
+                const Unit& u = c->units[l];
+                r.dst[r.n] = c->f32_of(me, u.off_grad, u);
+                r.slot0[r.n] = c->slot_of(me, u, 0);
+                r.slot_stride[r.n] = u.slot_stride / 4;
+                r.elems[r.n] = u.len(me);
+                r.marks[r.n] = c->mark_of(me, static_cast<int>(l), 0);
+                if (++r.n == odc::kMaxReduceUnits) {
+                    cuda_ok(odc::launch_slot_reduce(r, S(stream)), "slot reduce");
+                    r.n = 0;
+                }
             }
-            std::fill(c->pushed.begin(), c->pushed.end(), 0);
-            // every client's slot of this minibatch is read: clients may overwrite them
+            cuda_ok(odc::launch_slot_reduce(r, S(stream)), "slot reduce");
+            std::fill(c->touched.begin(), c->touched.end(), 0);
+            // the slots of this minibatch are consumed: clients may store into them again
             cuda_ok(odc::launch_publish(c->drain_of(me), c->mb_epoch, S(stream)), "publish drain epoch");
         }
         if (c->red_mode()) c->grads_pending = true;

@@ -96,6 +96,12 @@ struct Args {
     int tiles_m, tiles_n;
     int splits;  // split-K factor (fp32 output only): partial tiles are red.add-ed into D
     int group;   // raster: M-tiles per group (N swept inside a group); see raster_group()
+    // fused SwiGLU (gate_up projection, 2-CTA kernel only): B = [gate; up] (2*ffn rows); output tile n
+    // pairs gate rows [128n, 128n+128) (leader CTA's B half) with up rows ffn + [128n, 128n+128) (peer's),
+    // so one TMEM row holds g and u of the same 128 ffn columns. D = gu [M][2*ffn] as unfused,
+    // glu_m = silu(g) * u [M][ffn] (from the bf16-rounded g, u: bit-identical to swiglu_fwd)
+    void* glu_m;
+    int ffn;
 };
 
 // Tile raster (L2 reuse). Tiles are walked in groups of `group` M-tiles, the
@@ -500,7 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 coords(w / g.splits, m0, n0);
                 const int sp = w % g.splits;
                 const int kb = k_tiles * sp / g.splits, ke = k_tiles * (sp + 1) / g.splits;
-                const int ma = m0 + static_cast<int>(rank) * 128, nb = n0 + static_cast<int>(rank) * 128;
+                const int ma = m0 + static_cast<int>(rank) * 128;
+                const int nb = g.glu_m ? (rank ? g.ffn : 0) + n0 / 2 : n0 + static_cast<int>(rank) * 128;
                 for (int kt = kb; kt < ke; ++kt, ++it) {
                     const int s = it % kStages2;
                     if (it >= kStages2) mbar_wait(&empty_bar[s], ((it / kStages2) - 1) & 1);
@@ -586,6 +593,55 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             : (g.accumulate ? orow : nullptr);
             const bool fast = !g.d_f32 && n0 + BN2 <= g.N && (reinterpret_cast<uintptr_t>(orow) & 15) == 0 &&
                               (arow == nullptr || (reinterpret_cast<uintptr_t>(arow) & 15) == 0);
+            if (g.glu_m) {  // fused SwiGLU (host guarantees the fast-path conditions)
+                mbar_wait(&tmem_full[acc], use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned tbase = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2);
+                __nv_bfloat16* grow = static_cast<__nv_bfloat16*>(g.D) + row * g.ldd + n0 / 2;
+                __nv_bfloat16* urow = grow + g.ffn;
+                __nv_bfloat16* mrow = static_cast<__nv_bfloat16*>(g.glu_m) + row * g.ffn + n0 / 2;
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    unsigned ra[32], rb[32];
+                    tmem_ld32(tbase + c * 32, ra);        // gate columns
+                    tmem_ld32(tbase + 128 + c * 32, rb);  // up columns
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    reg_fence32(ra);
+                    reg_fence32(rb);
+                    if (c == 3) {  // accumulator in registers: release the buffer to the leader's MMA
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                             leader_empty0 + 8u * acc)
+                                         : "memory");
+                    }
+                    if (!row_ok) continue;
+#pragma unroll
+                    for (int q = 0; q < 32; q += 8) {
+                        uint4 vg, vu, vm;
+                        unsigned* wg = reinterpret_cast<unsigned*>(&vg);
+                        unsigned* wu = reinterpret_cast<unsigned*>(&vu);
+                        unsigned* wm = reinterpret_cast<unsigned*>(&vm);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            __nv_bfloat162 hg = __floats2bfloat162_rn(__uint_as_float(ra[q + 2 * e]), __uint_as_float(ra[q + 2 * e + 1]));
+                            __nv_bfloat162 hu = __floats2bfloat162_rn(__uint_as_float(rb[q + 2 * e]), __uint_as_float(rb[q + 2 * e + 1]));
+                            wg[e] = *reinterpret_cast<unsigned*>(&hg);
+                            wu[e] = *reinterpret_cast<unsigned*>(&hu);
+                            const float g0 = __low2float(hg), g1 = __high2float(hg);  // swiglu_fwd_kernel's formula
+                            const float m0v = __fdividef(g0, 1.f + __expf(-g0)) * __low2float(hu);
+                            const float m1v = __fdividef(g1, 1.f + __expf(-g1)) * __high2float(hu);
+                            __nv_bfloat162 hm = __floats2bfloat162_rn(m0v, m1v);
+                            wm[e] = *reinterpret_cast<unsigned*>(&hm);
+                        }
+                        *reinterpret_cast<uint4*>(grow + c * 32 + q) = vg;
+                        *reinterpret_cast<uint4*>(urow + c * 32 + q) = vu;
+                        *reinterpret_cast<uint4*>(mrow + c * 32 + q) = vm;
+                    }
+                }
+                continue;
+            }
             if (fast) {
                 uint4 cb[BN2 / 8];
                 if (arow && row_ok) {
@@ -805,6 +861,37 @@ cudaError_t launch(const void* A, const void* B, const Args& g, long long lda, l
 
 }  // namespace gemm
 }  // namespace odc
+
+extern "C" odc_status odc_gemm_gate_up_swiglu(const void* X, const void* W, void* gu, void* m, std::int64_t T,
+                                               std::int64_t ffn, std::int64_t d, void* stream) {
+    return odc::guard([&] {
+        using odcsim::ParamError;
+        if (T < 1 || ffn < 1 || d < 1) throw ParamError("gate_up: dims must be >= 1");
+        if (ffn % 128 || d % 8) throw ParamError("gate_up: ffn must be a multiple of 128 and d of 8");
+        if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16 ||
+            reinterpret_cast<uintptr_t>(gu) % 16 || reinterpret_cast<uintptr_t>(m) % 16)
+            throw ParamError("gate_up: operands must be 16-byte aligned");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (T < 256 || std::getenv("ODC_GEMM_1CTA")) {  // below one 2-CTA tile: the unfused sm_100a pair
+            const odc_status e = odc_gemm_bf16(X, W, gu, nullptr, T, 2 * ffn, d, d, d, 2 * ffn, 0, 0, ODC_BF16, 0, stream);
+            if (e != ODC_OK) throw std::runtime_error(odc_last_error());
+            const odc_status e2 = odc_w_swiglu_fwd(gu, m, T, static_cast<int>(ffn), stream);
+            if (e2 != ODC_OK) throw std::runtime_error(odc_last_error());
+            return;
+        }
+        odc::gemm::Args g{};
+        g.D = gu;
+        g.M = T;
+        g.N = 2 * ffn;
+        g.K = d;
+        g.ldd = 2 * ffn;
+        g.splits = 1;
+        g.glu_m = m;
+        g.ffn = static_cast<int>(ffn);
+        const cudaError_t e = odc::gemm::launch2(X, W, g, d, d, st);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("gate_up launch: ") + cudaGetErrorString(e));
+    });
+}
 
 extern "C" odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, std::int64_t M,
                                     std::int64_t N, std::int64_t K, std::int64_t lda, std::int64_t ldb, std::int64_t ldd,

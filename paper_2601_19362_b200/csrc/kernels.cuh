@@ -41,12 +41,15 @@ struct RedTable {
 struct BulkTable {
     int n = 0;
     const void* src[kMaxSeg];  // grad slice (fp32 or bf16)
-    void* dst[kMaxSeg];        // owner's int64 accumulator / fp32 grad shard (peer memory)
+    void* dst[kMaxSeg];        // owner's int64 accumulator / fp32 grad shard / fp32 slot (peer memory)
     std::int64_t elems[kMaxSeg];
     const unsigned long long* gate[kMaxSeg];
     unsigned long long need = 0;
     unsigned long long* err = nullptr;
     long long timeout_ns = 0;
+    bool assign[kMaxSeg] = {};                 // F32: store w*g instead of adding it (SLOT first push)
+    unsigned long long* mark[kMaxSeg] = {};    // optional: *mark[i] = mark_value (st.relaxed.sys, block 0)
+    unsigned long long mark_value = 0;
 };
 constexpr int kMaxFinal = 64;
 struct FixFinal {
@@ -73,21 +76,28 @@ cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s);
 cudaError_t launch_fetch_tma(const SegTable& t, int ctas, cudaStream_t s);
 // push, RED mode: remote red.relaxed.sys.global.add(.v4).f32 into owner shards
 cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas, cudaStream_t s);
-// push, SLOT mode (deterministic, local): acc[i] = (assign ? 0 : acc[i]) + w*g[i]
-// after every owner in `gates` reached `need` (previous reduce finished)
-cudaError_t launch_slot_accumulate(float* acc, const void* grad, bool src_bf16, std::int64_t n, float w, bool assign,
-                                   const unsigned long long* const* gates, int ngates, unsigned long long need,
-                                   unsigned long long* err, long long timeout_ns, int ctas, cudaStream_t s);
 // push through TMA bulk reductions (cp.reduce.async.bulk): FIXED mode
 // (deterministic, bounded memory) adds rn(w*g*scale) into every owner's int64
 // accumulator; otherwise (RED mode) w*g into the owner's fp32 grad shard
 cudaError_t launch_push_bulk(const BulkTable& t, bool fixed, float w, float scale, bool src_bf16, int ctas,
                              cudaStream_t s);
+// SLOT mode owner reduce (after the barrier): for every unit u,
+// dst[u][i] = sum over clients c (rank order) with marks[u][c] == epoch of
+// slot0[u][c * slot_stride[u] + i]; 0 if no client pushed the unit
+constexpr int kMaxReduceUnits = 48;
+struct SlotReduce {
+    int n = 0;
+    int nsrc = 0;
+    unsigned long long epoch = 0;
+    float* dst[kMaxReduceUnits];
+    const float* slot0[kMaxReduceUnits];
+    std::int64_t slot_stride[kMaxReduceUnits];
+    std::int64_t elems[kMaxReduceUnits];
+    const unsigned long long* marks[kMaxReduceUnits];
+};
+cudaError_t launch_slot_reduce(const SlotReduce& r, cudaStream_t s);
 // owner, after the barrier: grad[i] = fl(acc[i]) * inv_scale; acc[i] = 0
 cudaError_t launch_fixed_finalize(const FixFinal& f, float inv_scale, cudaStream_t s);
-// owner reduce in fixed source order: dst[i] = sum_{c=0..nsrc-1} src[c][i]
-cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc, std::int64_t n, int ctas,
-                                  cudaStream_t s);
 
 // ---- the generic typed kernels behind the reference-semantics fabric ----
 // dst[i] = dst[i] + w * src[i]   (one multiply, one add, each rounded; no FMA)

@@ -20,6 +20,12 @@
 //     fitting k — the reference's answer — is unchanged.
 #include <algorithm>
 #include <atomic>
+#include <charconv>
+#include <fstream>
+#include <istream>
+#include <sstream>
+#include <type_traits>
+#include <variant>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -195,6 +201,72 @@ Workload scale_lengths(const Workload& w, double ratio) {
     std::vector<Sample> s = w.samples();
     for (Sample& x : s) x.length = std::max<Tokens>(1, std::llround(static_cast<double>(x.length) * ratio));
     return Workload(std::move(s));
+}
+
+// "lognormal:mu=8,sigma=1.5" — the inverse of parse_dist_spec, numbers in the
+// stream's default (6 significant digits) format (src/workload.cpp:120-131)
+std::string format_dist_spec(const DistSpec& dist) {
+    std::ostringstream os;
+    std::visit(
+        [&](const auto& d) {
+            using D = std::decay_t<decltype(d)>;
+            if constexpr (std::is_same_v<D, LognormalDist>) os << "lognormal:mu=" << d.mu << ",sigma=" << d.sigma;
+            else if constexpr (std::is_same_v<D, ParetoDist>) os << "pareto:scale=" << d.scale << ",shape=" << d.shape;
+            else os << "uniform:lo=" << d.lo << ",hi=" << d.hi;
+        },
+        dist);
+    return os.str();
+}
+
+// one positive integer per line; whitespace-only lines skipped; anything else
+// is a FormatError naming its 1-based line (src/workload.cpp:145-169)
+Workload load_lengths(std::istream& in) {
+    std::vector<Sample> out;
+    std::string line;
+    for (std::int64_t no = 1; std::getline(in, line); ++no) {
+        const auto first = line.find_first_not_of(" \t\r");
+        if (first == std::string::npos) continue;
+        const auto last = line.find_last_not_of(" \t\r");
+        const char* b = line.data() + first;
+        const char* e = line.data() + last + 1;
+        Tokens v = 0;
+        const auto r = std::from_chars(b, e, v);
+        if (r.ec != std::errc() || r.ptr != e)
+            throw FormatError("line " + std::to_string(no) + ": not an integer: '" + std::string(b, e) + "'");
+        if (v < 1) throw FormatError("line " + std::to_string(no) + ": length must be positive, got " + std::to_string(v));
+        out.push_back(Sample{static_cast<std::int64_t>(out.size()), v});
+    }
+    if (out.empty()) throw FormatError("no lengths found in input");
+    return Workload(std::move(out));
+}
+
+Workload load_lengths_file(const std::string& path) {
+    std::ifstream f(path);
+    if (!f) throw FormatError("cannot open length file: " + path);
+    return load_lengths(f);
+}
+
+// count / min / max / exact total / mean and nearest-rank p50, p90, p99: the
+// smallest length with at least fraction p of the samples at or below it
+// (src/workload.cpp:187-214)
+WorkloadStats summarize(const Workload& w) {
+    std::vector<Tokens> v = w.lengths();
+    std::sort(v.begin(), v.end());
+    const auto n = static_cast<std::int64_t>(v.size());
+    auto rank = [&](double p) {
+        std::int64_t k = static_cast<std::int64_t>(std::ceil(p * static_cast<double>(n)));
+        return v[static_cast<std::size_t>(std::clamp<std::int64_t>(k, 1, n) - 1)];
+    };
+    WorkloadStats st;
+    st.count = n;
+    st.min = v.front();
+    st.max = v.back();
+    st.total = std::accumulate(v.begin(), v.end(), std::int64_t{0});
+    st.mean = static_cast<double>(st.total) / static_cast<double>(n);
+    st.p50 = rank(0.50);
+    st.p90 = rank(0.90);
+    st.p99 = rank(0.99);
+    return st;
 }
 
 // -------------------------------------------------------------- KK engine

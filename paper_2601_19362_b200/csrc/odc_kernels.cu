@@ -8,9 +8,11 @@
 //   push_red        push (a6), RED mode: red.relaxed.sys.global.add.v4.f32
 //                   straight into each owner's fp32 grad shard (NVLink).
 //                   replaces split_gradient + try_stage + consume :80-136
-//   slot_accumulate push (a6), SLOT mode: single-writer per-source slot
-//                   acc += w*g (local HBM), deterministic.
-//   reduce_sources  owner reduce in fixed rank order (SLOT mode barrier step)
+//   push_bulk       push (a6) through TMA bulk ops into peer HBM: RED (fp32
+//                   reductions into the owner's grad shard), SLOT (w*g stored,
+//                   then added, into this client's slot AT THE OWNER),
+//                   FIXED (int64 fixed-point reductions)
+//   slot_reduce     SLOT mode owner reduce in fixed rank order (barrier step)
 //   push_fixed      push (a6), FIXED mode: w*g rounded to int64 fixed point,
 //                   TMA bulk .add.u64 reductions into the owner (deterministic
 //                   in any order, 8 B per owned element); fixed_finalize
@@ -483,7 +485,7 @@ cudaError_t launch_push_red(const RedTable& t, float w, bool src_bf16, int ctas,
     return cudaGetLastError();
 }
 
-// ------------------------------------------------------------ push (SLOT)
+// ------------------------------------------------------------ gates
 struct GateList {
     const unsigned long long* g[kMaxSeg];
     int n;
@@ -499,101 +501,6 @@ __device__ __forceinline__ bool pass_gates(const GateList& gl) {
     if (threadIdx.x < gl.n && !wait_geq(gl.g[threadIdx.x], gl.need, gl.err, gl.timeout_ns)) ok = 0;
     __syncthreads();
     return ok != 0;
-}
-
-template <bool BF16, bool ASSIGN>
-__global__ void __launch_bounds__(512) slot_accumulate_kernel(float* __restrict__ acc, const void* __restrict__ grad,
-                                                               std::int64_t n, float w, GateList gl) {
-    if (gl.n > 0 && !pass_gates(gl)) return;
-    // acc and grad are both 16B/8B aligned at element 0 (full-layer buffers)
-    const std::int64_t units = n / 4;
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < units; u += stride) {
-        const float4 g = load_grad4<BF16>(grad, 4 * u);
-        float4 a = ASSIGN ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4*>(acc)[u];
-        a.x = __fadd_rn(a.x, __fmul_rn(w, g.x));
-        a.y = __fadd_rn(a.y, __fmul_rn(w, g.y));
-        a.z = __fadd_rn(a.z, __fmul_rn(w, g.z));
-        a.w = __fadd_rn(a.w, __fmul_rn(w, g.w));
-        reinterpret_cast<float4*>(acc)[u] = a;
-    }
-    if (blockIdx.x == 0 && threadIdx.x < n - 4 * units) {
-        const std::int64_t e = 4 * units + threadIdx.x;
-        acc[e] = __fadd_rn(ASSIGN ? 0.f : acc[e], __fmul_rn(w, load_grad<BF16>(grad, e)));
-    }
-}
-
-cudaError_t launch_slot_accumulate(float* acc, const void* grad, bool src_bf16, std::int64_t n, float w, bool assign,
-                                   const unsigned long long* const* gates, int ngates, unsigned long long need,
-                                   unsigned long long* err, long long timeout_ns, int ctas, cudaStream_t s) {
-    if (n <= 0) return cudaSuccess;
-    if (reinterpret_cast<uintptr_t>(acc) % 16 || reinterpret_cast<uintptr_t>(grad) % (src_bf16 ? 8 : 16))
-        return cudaErrorMisalignedAddress;
-    GateList gl{};
-    gl.n = ngates;
-    for (int i = 0; i < ngates; ++i) gl.g[i] = gates[i];
-    gl.need = need;
-    gl.err = err;
-    gl.timeout_ns = timeout_ns;
-    if (ctas <= 0) ctas = 296;
-    count_launch();
-    if (src_bf16) {
-        if (assign) slot_accumulate_kernel<true, true><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
-        else slot_accumulate_kernel<true, false><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
-    } else {
-        if (assign) slot_accumulate_kernel<false, true><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
-        else slot_accumulate_kernel<false, false><<<ctas, 512, 0, s>>>(acc, grad, n, w, gl);
-    }
-    return cudaGetLastError();
-}
-
-// owner-side fixed-order reduce of the per-source slots (peer loads)
-struct SrcList {
-    const float* p[kMaxSeg];
-    int n;
-};
-
-__global__ void __launch_bounds__(512) reduce_sources_kernel(float* __restrict__ dst, SrcList sl, std::int64_t n) {
-    // dst and every source are co-aligned (same element offset mod 4)
-    const unsigned h = static_cast<unsigned>((reinterpret_cast<uintptr_t>(dst) >> 2) & 3);
-    const std::int64_t head = i64min(n, (4 - h) & 3);
-    const std::int64_t units = (n - head) / 4;
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < units; u += stride) {
-        const std::int64_t e = head + 4 * u;
-        float4 a = *reinterpret_cast<const float4*>(sl.p[0] + e);
-        for (int c = 1; c < sl.n; ++c) {  // rank order 0..N-1: deterministic
-            const float4 b = *reinterpret_cast<const float4*>(sl.p[c] + e);
-            a.x = __fadd_rn(a.x, b.x);
-            a.y = __fadd_rn(a.y, b.y);
-            a.z = __fadd_rn(a.z, b.z);
-            a.w = __fadd_rn(a.w, b.w);
-        }
-        *reinterpret_cast<float4*>(dst + e) = a;
-    }
-    if (blockIdx.x == 0) {
-        const std::int64_t tail = n - head - 4 * units;
-        int e = -1;
-        if (threadIdx.x < head) e = threadIdx.x;
-        else if (threadIdx.x >= 4 && threadIdx.x < 4 + tail) e = static_cast<int>(head + 4 * units + threadIdx.x - 4);
-        if (e >= 0) {
-            float a = sl.p[0][e];
-            for (int c = 1; c < sl.n; ++c) a = __fadd_rn(a, sl.p[c][e]);
-            dst[e] = a;
-        }
-    }
-}
-
-cudaError_t launch_reduce_sources(float* dst, const float* const* srcs, int nsrc, std::int64_t n, int ctas,
-                                  cudaStream_t s) {
-    if (n <= 0 || nsrc <= 0) return cudaSuccess;
-    SrcList sl{};
-    sl.n = nsrc;
-    for (int i = 0; i < nsrc; ++i) sl.p[i] = srcs[i];
-    if (ctas <= 0) ctas = 296;
-    count_launch();
-    reduce_sources_kernel<<<ctas, 512, 0, s>>>(dst, sl, n);
-    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ push (FIXED)
@@ -635,11 +542,14 @@ __device__ __forceinline__ float2 load_grad2(const void* src, std::int64_t e) {
     }
 }
 
-// One kernel body for both bulk pushes: every 16 B unit of the owner's shard
+// One kernel body for the bulk pushes: every 16 B unit of the owner's shard
 // (FIXED: 2 int64, F32: 4 fp32) is produced in registers, staged in a 3-deep
 // shared-memory ring and added into peer HBM by one elected thread with
-// cp.reduce.async.bulk (.add.u64 / .add.f32). 8 KB per bulk op, 25 KB of
-// smem per CTA so four CTAs share an SM (and one fits next to a GEMM).
+// cp.reduce.async.bulk (.add.u64 / .add.f32) — or, for an F32 segment marked
+// `assign` (SLOT mode: the first push of a unit into this client's slot at the
+// owner in this minibatch), STORED with cp.async.bulk (NVLink write
+// bandwidth, no remote read-modify-write). 8 KB per bulk op, 25 KB of smem per
+// CTA so four CTAs share an SM (and one fits next to a GEMM).
 constexpr int kBulkUnits = 2;   // 16 B units per thread per chunk
 constexpr int kBulkStages = 3;
 
@@ -655,9 +565,12 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
     bool range = false, under = false;  // FIXED conversion flags of this thread
     if (threadIdx.x == 0) gate_ok = 1;
     __syncthreads();
-    // FIXED: the owner drained its accumulator at its last minibatch end; F32: the owner's AdamW zeroed its grad shard
-    if (threadIdx.x < t.n && t.gate[threadIdx.x] && !wait_geq(t.gate[threadIdx.x], t.need, t.err, t.timeout_ns))
-        gate_ok = 0;
+    // the owner consumed what the previous minibatch left in this push target (drain epoch)
+    const bool my_gate = !(threadIdx.x < t.n && t.gate[threadIdx.x]) ||
+                         wait_geq(t.gate[threadIdx.x], t.need, t.err, t.timeout_ns);
+    if (!my_gate) gate_ok = 0;
+    if (my_gate && blockIdx.x == 0 && threadIdx.x < t.n && t.mark[threadIdx.x])  // SLOT: "client pushed this unit"
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(t.mark[threadIdx.x]), "l"(t.mark_value) : "memory");
     if (threadIdx.x < t.n) {
         const int i = threadIdx.x;
         // the owner's shard is co-aligned with its position in the caller's full-layer
@@ -720,6 +633,10 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
                     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
                                  "r"(src), "r"(bytes)
                                  : "memory");
+                else if (t.assign[i])
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                                 "r"(bytes)
+                                 : "memory");
                 else
                     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
                                  "r"(src), "r"(bytes)
@@ -736,6 +653,7 @@ __global__ void __launch_bounds__(kFixThreads) push_bulk_kernel(BulkTable t, flo
     auto scalar = [&](int i, std::int64_t e) {
         const float g = load_grad<BF16>(t.src[i], e);
         if constexpr (FIXED) red_sys_u64(static_cast<long long*>(t.dst[i]) + e, to_fixed(w, g, scale, range, under));
+        else if (t.assign[i]) static_cast<float*>(t.dst[i])[e] = __fmul_rn(w, g);
         else red_sys_f32(static_cast<float*>(t.dst[i]) + e, __fmul_rn(w, g));
     };
     for (int i = 0; i < t.n; ++i)  // segments whose src/dst alignment rules out the bulk path: scalar reductions
@@ -771,6 +689,70 @@ cudaError_t launch_push_bulk(const BulkTable& t, bool fixed, float w, float scal
         if (src_bf16) push_bulk_kernel<true, false><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
         else push_bulk_kernel<false, false><<<ctas, kFixThreads, 0, s>>>(t, w, scale);
     }
+    return cudaGetLastError();
+}
+
+// SLOT mode, owner side, after the minibatch barrier: every unit's grad shard
+// = the clients' slots summed in fixed rank order 0..N-1, counting only the
+// clients whose mark says they pushed the unit in this minibatch (a slot that
+// was not written this minibatch still holds an older one). Local HBM only:
+// the slots were written over NVLink during the clients' backward passes.
+__global__ void __launch_bounds__(512) slot_reduce_kernel(SlotReduce r) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (int u = 0; u < r.n; ++u) {
+        const std::int64_t n = r.elems[u];
+        if (n <= 0) continue;
+        unsigned active = 0;  // clients that pushed this unit (N <= kMaxSeg)
+        for (int c = 0; c < r.nsrc; ++c)
+            if (*reinterpret_cast<volatile const unsigned long long*>(r.marks[u] + c) == r.epoch) active |= 1u << c;
+        float* dst = r.dst[u];
+        const float* s0 = r.slot0[u];
+        const std::int64_t sst = r.slot_stride[u];
+        const unsigned h = static_cast<unsigned>((reinterpret_cast<uintptr_t>(dst) >> 2) & 3);
+        const std::int64_t head = i64min(n, (4 - h) & 3);
+        const std::int64_t units = (n - head) / 4;
+        for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < units; k += stride) {
+            const std::int64_t e = head + 4 * k;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+            bool first = true;
+            for (int c = 0; c < r.nsrc; ++c) {  // rank order: deterministic
+                if (!(active >> c & 1u)) continue;
+                const float4 b = *reinterpret_cast<const float4*>(s0 + c * sst + e);
+                if (first) {
+                    a = b;
+                    first = false;
+                } else {
+                    a.x = __fadd_rn(a.x, b.x);
+                    a.y = __fadd_rn(a.y, b.y);
+                    a.z = __fadd_rn(a.z, b.z);
+                    a.w = __fadd_rn(a.w, b.w);
+                }
+            }
+            *reinterpret_cast<float4*>(dst + e) = a;
+        }
+        if (blockIdx.x == 0) {  // ragged head / tail
+            const std::int64_t tail = n - head - 4 * units;
+            std::int64_t e = -1;
+            if (threadIdx.x < head) e = threadIdx.x;
+            else if (threadIdx.x >= 4 && threadIdx.x < 4 + tail) e = head + 4 * units + threadIdx.x - 4;
+            if (e >= 0) {
+                float a = 0.f;
+                bool first = true;
+                for (int c = 0; c < r.nsrc; ++c) {
+                    if (!(active >> c & 1u)) continue;
+                    a = first ? s0[c * sst + e] : __fadd_rn(a, s0[c * sst + e]);
+                    first = false;
+                }
+                dst[e] = a;
+            }
+        }
+    }
+}
+
+cudaError_t launch_slot_reduce(const SlotReduce& r, cudaStream_t s) {
+    if (r.n <= 0) return cudaSuccess;
+    count_launch();
+    slot_reduce_kernel<<<148 * 2, 512, 0, s>>>(r);
     return cudaGetLastError();
 }
 

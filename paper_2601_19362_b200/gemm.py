@@ -76,3 +76,23 @@ def linear_wgrad(dy, x, out=None, accumulate=False):
     K_in = x.shape[1]
     out = torch.empty(N_out, K_in, dtype=torch.float32, device=dy.device) if out is None else out
     return gemm(dy, x, out, N_out, K_in, T, dy.stride(0), x.stride(0), 1, 1, accumulate=accumulate)
+
+
+def gate_up_swiglu(x, w, ffn):
+    """gu = x·wᵀ (w = [gate; up], [2*ffn, d]) and m = silu(gate)·up fused in the
+    GEMM epilogue (csrc/gemm.cu glu mode). Returns (gu [T, 2*ffn], m [T, ffn])."""
+    T, d = x.shape
+    assert w.shape == (2 * ffn, d) and x.is_contiguous() and w.is_contiguous()
+    gu = torch.empty(T, 2 * ffn, dtype=torch.bfloat16, device=x.device)
+    m = torch.empty(T, ffn, dtype=torch.bfloat16, device=x.device)
+    s = torch.cuda.current_stream()
+    rec = recorder
+    if rec is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+    check(lib().odc_gemm_gate_up_swiglu(_p(x), _p(w), _p(gu), _p(m), T, ffn, d, C.c_void_p(s.cuda_stream)))
+    if rec is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(s)
+        rec.rows.append((2.0 * T * 2 * ffn * d, e0, e1, (T, 2 * ffn, d, 0, 0, False, False, "glu")))
+    return gu, m

@@ -370,8 +370,7 @@ class Worker:
             o, lse = F.attn_fwd(q, k, v, b.attn_items, 1.0 / math.sqrt(hd))
         hm = G.linear_fwd(o.view(T, H * hd), P["o_w"], residual=x)
         bn, r2 = F.rmsnorm_fwd(hm, P["ln2"])
-        gu = G.linear_fwd(bn, P["gu_w"])
-        m = F.swiglu_fwd(gu, s.ffn)
+        gu, m = G.gate_up_swiglu(bn, P["gu_w"], s.ffn)  # SwiGLU fused into the GEMM epilogue
         h = G.linear_fwd(m, P["down_w"], residual=hm) if out else None
         return (x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m), h
 

@@ -4,6 +4,14 @@ import sys
 
 import pytest
 
+# Several ODC ranks in ONE process (OdcEngine.local_group, config0) wait on one
+# another's device flags from different streams. CUDA maps streams onto
+# CUDA_DEVICE_MAX_CONNECTIONS hardware work queues (default 8); two ranks'
+# streams sharing a queue serialise, so rank a's spinning barrier kernel would
+# block rank b's kernels queued behind it. 32 queues give every stream these
+# tests create its own. Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

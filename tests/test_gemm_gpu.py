@@ -56,3 +56,19 @@ def test_bf16_accumulate_in_place():
     want = x.float() @ w.float().t() + y.float()
     G.gemm(x, w, y, T, out, inn, x.stride(0), w.stride(0), False, False, accumulate=True)
     torch.testing.assert_close(y.float(), want, rtol=1e-2, atol=2e-2 * (inn / 64) ** 0.5)
+
+
+@pytest.mark.parametrize("T,d,ffn", [(100, 256, 512), (1000, 1536, 8960), (4097, 512, 1024), (32768, 1536, 8960)])
+def test_gate_up_swiglu_fused_matches_unfused(T, d, ffn):
+    """SwiGLU fused into the gate_up GEMM epilogue: gu bit-identical to the
+    plain GEMM, m bit-identical to the standalone swiglu kernel on that gu
+    (T < 256 runs the unfused pair itself)."""
+    from paper_2601_19362_b200 import fused as F
+
+    x, w = _r(T, d), (torch.randn(2 * ffn, d, device=DEV) * 0.05).to(torch.bfloat16)
+    gu, m = G.gate_up_swiglu(x, w, ffn)
+    gu_ref = G.linear_fwd(x, w)
+    assert torch.equal(gu, gu_ref)
+    assert torch.equal(m, F.swiglu_fwd(gu_ref, ffn))
+    g, u = gu_ref.float()[:, :ffn], gu_ref.float()[:, ffn:]
+    torch.testing.assert_close(m.float(), torch.nn.functional.silu(g) * u, rtol=2e-2, atol=2e-2)

@@ -42,3 +42,15 @@ def test_reference_partition_tests_pass_on_b200_lb():
 def test_reference_primitives_tests_pass_on_gpu_fabric():
     out = _run(_binary("ref_primitives_tests"))
     assert "test cases: 13" in out or "test cases: 14" in out
+
+
+def test_reference_workload_tests_pass_on_facade():
+    """tests/test_workload.cpp (generators, length files, scaling, summarize,
+    dist-spec strings) against include/odcsim/workload.hpp + libodc.so."""
+    out = _run(_binary("ref_workload_tests"))
+    assert "test cases: 16" in out
+
+
+def test_reference_cost_model_tests_pass_on_facade():
+    out = _run(_binary("ref_cost_model_tests"))
+    assert "test cases: 9" in out
