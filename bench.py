@@ -51,8 +51,8 @@ METRIC = "tokens/sec at 1/2/4/8 B200 on long-tail seq lengths; fetch/push GB/s v
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="odc", choices=["odc", "reference"])
     ap.add_argument("--workload", default="sft", choices=["sft", "odc_minibatch_comm"])
     ap.add_argument("--no-fsdp", action="store_true", help="skip the same-box NCCL FSDP comparison arm")

@@ -230,6 +230,10 @@ odc_status odc_gemm_bf16(const void* A, const void* B, void* D, const void* C, i
                          int64_t lda, int64_t ldb, int64_t ldd, int a_mn_major, int b_mn_major, int d_dtype,
                          int accumulate, void* stream);
 
+/* GEMM tile raster (L2 reuse; tuning / A-B only): group = M-tiles per raster
+ * group (0 = automatic from the L2 budget), l2_budget_mb (0 = keep). */
+odc_status odc_gemm_set_raster(int group, int l2_budget_mb);
+
 /* gate/up projection with SwiGLU fused into the epilogue (2-CTA tcgen05 GEMM):
  * gu [T][2*ffn] = X [T][d] · W^T with W = [gate; up] [2*ffn][d] (as odc_gemm_bf16),
  * and m [T][ffn] = silu(gate) * up computed from the bf16-rounded gu values

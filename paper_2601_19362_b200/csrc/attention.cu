@@ -26,7 +26,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -523,11 +522,6 @@ __device__ __forceinline__ void stage_f32(char* stage, int r, int c0, const unsi
     }
 }
 
-// dQ of an iteration leaves the SM either through a 64 KB fp32 smem staging
-// (aliasing sP / sdS) and a TMA reduce-add (DQ_RED = false), or straight from
-// the elementwise warps' registers as red.global.add.v4.f32 (DQ_RED = true: no
-// staging, so P/dS of the next iteration never wait for a drain).
-template <bool DQ_RED>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
@@ -541,14 +535,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     char* sdO = smem + 4 * kTile;
     char* sP = smem + 5 * kTile;
     char* sdS = smem + 6 * kTile;
-    char* stage = sP;  // [sP, sdS] = 64 KB fp32 staging of dQ_n (DQ_RED = false)
-    // Two elementwise phases per iteration n, each handing the tensor core work as soon as it is done:
-    //   s_full:  S_n in TMEM                      s_read:  S_n in registers (S columns free for S_{n+1})
-    //   dp_full: dP_n in TMEM                     p_full:  P_n in smem (dV_n may run)
-    //   ds_full: dS_n in smem (dK_n, dQ_n may run; dP_n was read before)
-    //   dq_full: every MMA of n done (dQ_n in the dP columns)   dq_read: dQ_n read out (dP columns free)
-    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, s_full, s_read,
-        dp_full, p_full, ds_full, dq_full, dq_read;
+    char* stage = sP;  // [sP, sdS] = 64 KB fp32 staging of dQ_n once every MMA of n is done
+    // sdp_full: S_n and dP_n in TMEM; ds_full: P_n / dS_n in smem (S_n, dP_n consumed);
+    // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
+    // s_read: S_n, dP_n are in the elementwise warps' registers (S columns free for S_{n+1})
+    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, s_read,
+        ds_full, dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
     const BwdItem it = g.items[blockIdx.x];
@@ -569,10 +561,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         mbar_init(&do_full, 1);
         mbar_init(&do_empty, 1);
-        mbar_init(&s_full, 1);
+        mbar_init(&sdp_full, 1);
         mbar_init(&s_read, 8);
-        mbar_init(&dp_full, 1);
-        mbar_init(&p_full, 8);
+#ifdef ODC_ATTN_DEBUG
+        if (blockIdx.x == 0)
+            printf("bars: kv_full %x q_full %x %x q_empty %x %x do_full %x do_empty %x sdp_full %x s_read %x ds_full %x "
+                   "dq_full %x dq_read %x n_iter %d\n",
+                   su32(&kv_full), su32(&q_full[0]), su32(&q_full[1]), su32(&q_empty[0]), su32(&q_empty[1]),
+                   su32(&do_full), su32(&do_empty), su32(&sdp_full), su32(&s_read), su32(&ds_full), su32(&dq_full),
+                   su32(&dq_read), it.it_end - it.it_begin);
+#endif
         mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
         mbar_init(&dq_read, 8);
@@ -613,7 +611,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer: dP_n, [P_n] dV_n, S_{n+1}, [dS_n] dK_n, dQ_n
+        if (lane == 0) {  // ---- MMA issuer
             const unsigned id_kk = instr(0, 0), id_mm = instr(1, 1), id_km = instr(0, 1);
             mbar_wait(&kv_full, 0);
             const unsigned doa = su32(sdO), ka = su32(sK), va = su32(sV), pa = su32(sP), dsa = su32(sdS);
@@ -627,7 +625,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_S, sdesc(qa + off, 16, 1024), sdesc(ka + off, 16, 1024), id_kk, kk > 0);
                 }
-                commit(&s_full);
             };
             issue_s(0);
             for (int n = 0; n < n_iter; ++n) {
@@ -641,20 +638,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_DP, sdesc(doa + off, 16, 1024), sdesc(va + off, 16, 1024), id_kk, kk > 0);
                 }
-                commit(&dp_full);
-                mbar_wait(&p_full, n & 1);  // P_n in smem (its phase needed only S_n)
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-                for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO; K = query rows: MN-major A (P^T) and B (dO)
-                    mma(tmem + T_DV, sdesc(pa + kk * 2048, kTile / 2, 1024), sdesc(doa + kk * 2048, kTile / 2, 1024),
-                        id_mm, (n > 0 || kk > 0));
-                commit(&do_empty);  // dO_n consumed: the TMA refills it while the rest runs
-                if (n + 1 < n_iter) {  // S columns were read out before P_n was stored
+                commit(&sdp_full);
+                if (n + 1 < n_iter) {  // S_{n+1} overlaps the elementwise work of n once S_n is in registers
                     mbar_wait(&s_read, n & 1);
                     issue_s(n + 1);
                 }
-                mbar_wait(&ds_full, n & 1);  // dS in smem
+                mbar_wait(&ds_full, n & 1);  // P, dS in smem
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk)  // K = query rows: MN-major A (P^T) and B (dO)
+                    mma(tmem + T_DV, sdesc(pa + kk * 2048, kTile / 2, 1024), sdesc(doa + kk * 2048, kTile / 2, 1024),
+                        id_mm, (n > 0 || kk > 0));
+                commit(&do_empty);  // dO_n consumed: the TMA refills it while dK, dQ run
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
                     mma(tmem + T_DK, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024),
@@ -671,6 +666,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     } else {  // ---- elementwise / dQ / dK dV epilogue: row quadrant warp%4, column half
         asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+#ifdef ODC_ATTN_DEBUG
+        if (lane == 0 && blockIdx.x == 0) printf("ew warp %d start\n", warp);
+#endif
         const int quad = warp % 4;
         const int c0 = ((warp - 4) >> 2) * 64;  // this warp's 64 columns
         const bool lead = warp == 4 && lane == 0;  // issues the TMA reductions
@@ -695,66 +693,59 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const float Ds = d_nx * sc;
             stats(n + 1, lse_nx, d_nx);
             const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV - c0 : -1;  // visible keys among our columns
-            // ---- phase 1 (needs S_n only; overlaps dP_n on the tensor core): P = exp2(S*scale*log2e - lse2)
-            mbar_wait(&s_full, n & 1);
+            mbar_wait(&sdp_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            unsigned sv[64];
+            unsigned sv[64], dp[64];
             TM_LD32(tmem + lane_base + T_S + c0, sv);
             TM_LD32(tmem + lane_base + T_S + c0 + 32, (sv + 32));
+            TM_LD32(tmem + lane_base + T_DP + c0, dp);
+            TM_LD32(tmem + lane_base + T_DP + c0 + 32, (dp + 32));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_read);
+#ifdef ODC_ATTN_DEBUG
+            if (lane == 0 && blockIdx.x == 0) printf("ew warp %d n %d s_read\n", warp, n);
+#endif
+            // P = exp2(S*scale*log2e - lse2) (0 where masked), dS = P * (dP*scale - D*scale), packed bf16 in
+            // place; packed fp32x2 math, and no mask work on tiles this row sees entirely
             const float2 v_sl2 = make_float2(sl2, sl2), v_nlse = make_float2(-lse2, -lse2);
-            float pf[64];  // P in fp32 (in place of S) for phase 2
+            const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
+            if (lim >= 63) {
 #pragma unroll
-            for (int x = 0; x < 64; x += 2) {
-                const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
-                // one pair in two through the FMA-pipe exp2: MUFU alone would need 1,024 clk per iteration
-                float2 pp = ((x >> 1) & 1) ? ex2_fma2(t) : make_float2(ex2(t.x), ex2(t.y));
-                if (lim < 63) {
-                    if (x > lim) pp.x = 0.f;
-                    if (x + 1 > lim) pp.y = 0.f;
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
+                    const float2 pp = make_float2(ex2(t.x), ex2(t.y));
+                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
+                    const float2 d = fmul2(pp, u);
+                    sv[x / 2] = pack_bf16(pp.x, pp.y);
+                    dp[x / 2] = pack_bf16(d.x, d.y);
                 }
-                pf[x] = pp.x;
-                pf[x + 1] = pp.y;
+            } else {
+#pragma unroll
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
+                    const float2 pp = make_float2(x > lim ? 0.f : ex2(t.x), x + 1 > lim ? 0.f : ex2(t.y));
+                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
+                    const float2 d = fmul2(pp, u);
+                    sv[x / 2] = pack_bf16(pp.x, pp.y);
+                    dp[x / 2] = pack_bf16(d.x, d.y);
+                }
             }
-            if (!DQ_RED && n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
+            if (n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
                 if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 bar_ew();
             }
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                unsigned pk[16];
-#pragma unroll
-                for (int x = 0; x < 32; x += 2) pk[x / 2] = pack_bf16(pf[32 * hh + x], pf[32 * hh + x + 1]);
-                store_swizzled(sP, r, c0 + 32 * hh, pk);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full);
-            // ---- phase 2 (needs dP_n; overlaps dV_n and S_{n+1}): dS = P * (dP*scale - D*scale)
-            mbar_wait(&dp_full, n & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time (register pressure)
-                unsigned dp[32], pk[16];
-                TM_LD32(tmem + lane_base + T_DP + c0 + 32 * hh, dp);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int x = 0; x < 32; x += 2) {
-                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
-                    const float2 d = fmul2(make_float2(pf[32 * hh + x], pf[32 * hh + x + 1]), u);
-                    pk[x / 2] = pack_bf16(d.x, d.y);
-                }
-                store_swizzled(sdS, r, c0 + 32 * hh, pk);
-            }
+            store_swizzled(sP, r, c0, sv);
+            store_swizzled(sP, r, c0 + 32, sv + 16);
+            store_swizzled(sdS, r, c0, dp);
+            store_swizzled(sdS, r, c0 + 32, dp + 16);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&ds_full);
-            // ---- dQ_n (fp32, already scaled) -> the global accumulator, while the MMA warp starts dP_{n+1}
+            // dQ_n (fp32, already scaled) -> smem staging -> TMA reduce-add into the global accumulator,
+            // while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             unsigned v[64];
@@ -764,28 +755,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&dq_read);
-            if constexpr (DQ_RED) {
-                if (q_ok) {  // rows past the sequence end belong to the next sequence (or past T)
-                    float* row = g.dq_acc + ((static_cast<long long>(it.seq_start) + qi) * g.H + h) * HD + c0;
+            stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_ew();
+            if (lead) {
+                const int row0 = it.seq_start + i * BQ;
 #pragma unroll
-                    for (int x = 0; x < 64; x += 4)
-                        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + x),
-                                     "f"(__uint_as_float(v[x])), "f"(__uint_as_float(v[x + 1])),
-                                     "f"(__uint_as_float(v[x + 2])), "f"(__uint_as_float(v[x + 3]))
-                                     : "memory");
+                for (int k = 0; k < 4; ++k) {
+                    tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
                 }
-            } else {
-                stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bar_ew();
-                if (lead) {
-                    const int row0 = it.seq_start + i * BQ;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
-                    }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
         // dK, dV of the key tile (complete: the last dq_full covers every MMA) -> staging -> TMA reduce-add
@@ -953,9 +932,7 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
         int dev = 0;
         cudaGetDevice(&dev);
         if (configured != dev) {
-            cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(attn_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+            cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
             if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
@@ -992,13 +969,7 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
-            // dQ path: ODC_ATTN_DQ=red (registers -> red.global.add.v4) | tma (smem staging + TMA reduce-add)
-            static const bool dq_red = [] {
-                const char* v = std::getenv("ODC_ATTN_DQ");
-                return !(v && std::string(v) == "tma");
-            }();
-            if (dq_red) attn_bwd_kernel<true><<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
-            else attn_bwd_kernel<false><<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
+            attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
         auto convert = [&](const float* acc, void* out, long long n) {
             odc::count_launch();

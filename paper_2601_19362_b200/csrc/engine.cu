@@ -291,6 +291,7 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
             c->arena_bytes = off;
             c->layout_hash = h;
             c->dev();
+            cuda_ok(odc::preload_kernels(), "preload kernels");
             cuda_ok(cudaMalloc(&c->arena, static_cast<std::size_t>(off)), "cudaMalloc arena");
             cuda_ok(cudaMemset(c->arena, 0, static_cast<std::size_t>(off)), "memset arena");
             // the zeroed flags page must be visible before the arena is exported: peers poll it over NVLink

@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -113,15 +114,25 @@ struct Args {
 // L2 (the gate_up weight, 55 MB, is then read ~3x at 32K tokens instead of
 // 16x with a fixed group of 8). ODC_GEMM_GROUP forces a group,
 // ODC_GEMM_L2_MB sets the budget (default 40 MB of the 126 MB L2).
+// process-wide raster settings (ODC_GEMM_GROUP / ODC_GEMM_L2_MB at first use;
+// odc_gemm_set_raster overrides them, for interleaved A/B timing)
+inline std::atomic<int>& raster_forced() {
+    static std::atomic<int> v{[] {
+        const char* e = std::getenv("ODC_GEMM_GROUP");
+        return e ? std::atoi(e) : 0;
+    }()};
+    return v;
+}
+inline std::atomic<long long>& raster_budget() {
+    static std::atomic<long long> v{[] {
+        const char* e = std::getenv("ODC_GEMM_L2_MB");
+        return (e ? std::atoll(e) : 40LL) << 20;
+    }()};
+    return v;
+}
 inline int raster_group(long long K, int tiles_m, int tiles_n, int tile_rows_a, int tile_rows_b) {
-    static const int forced = [] {
-        const char* v = std::getenv("ODC_GEMM_GROUP");
-        return v ? std::atoi(v) : 0;
-    }();
-    static const long long budget = [] {
-        const char* v = std::getenv("ODC_GEMM_L2_MB");
-        return (v ? std::atoll(v) : 40LL) << 20;
-    }();
+    const int forced = raster_forced().load(std::memory_order_relaxed);
+    const long long budget = raster_budget().load(std::memory_order_relaxed);
     if (forced > 0) return forced < tiles_m ? forced : tiles_m;
     const long long a_tile = static_cast<long long>(tile_rows_a) * K * 2, b_tile = static_cast<long long>(tile_rows_b) * K * 2;
     if (b_tile * tiles_n <= budget) return 1;
@@ -861,6 +872,14 @@ cudaError_t launch(const void* A, const void* B, const Args& g, long long lda, l
 
 }  // namespace gemm
 }  // namespace odc
+
+extern "C" odc_status odc_gemm_set_raster(int group, int l2_budget_mb) {
+    return odc::guard([&] {
+        if (group < 0 || l2_budget_mb < 0) throw odcsim::ParamError("raster: group and budget must be >= 0");
+        odc::gemm::raster_forced().store(group);
+        if (l2_budget_mb > 0) odc::gemm::raster_budget().store(static_cast<long long>(l2_budget_mb) << 20);
+    });
+}
 
 extern "C" odc_status odc_gemm_gate_up_swiglu(const void* X, const void* W, void* gu, void* m, std::int64_t T,
                                                std::int64_t ffn, std::int64_t d, void* stream) {

@@ -149,6 +149,8 @@ struct AdamArgs {
 cudaError_t launch_adam(const AdamArgs& a, std::int64_t total_vec_units, int ctas, cudaStream_t s);
 
 cudaError_t launch_l2_flush(void* scratch, std::int64_t bytes, cudaStream_t s);
+// force-load every protocol kernel into the current context (see odc_kernels.cu)
+cudaError_t preload_kernels();
 // owner init: master[i] = src[i]; param[i] = bf16_rn(src[i])
 cudaError_t launch_init_shard(float* master, unsigned short* param, const float* src, std::int64_t n, cudaStream_t s);
 

@@ -1016,6 +1016,31 @@ __global__ void init_shard_kernel(float* master, unsigned short* param, const fl
     }
 }
 
+// Loads every kernel of the ODC protocol into the context up front. With CUDA's
+// lazy module loading, the FIRST launch of a kernel may wait for the device's
+// running work; when that work is a barrier spinning on a peer whose kernels
+// this host thread has yet to launch (several ranks driven from one thread,
+// odc_ctx_import_ctx), the host would block inside the launch and the barrier
+// would only end by its watchdog. Also keeps first-launch latency out of timed steps.
+cudaError_t preload_kernels() {
+    const void* fns[] = {
+        reinterpret_cast<const void*>(copy_segments_kernel), reinterpret_cast<const void*>(fetch_tma_kernel),
+        reinterpret_cast<const void*>(push_red_kernel<true>), reinterpret_cast<const void*>(push_red_kernel<false>),
+        reinterpret_cast<const void*>(push_bulk_kernel<true, true>),
+        reinterpret_cast<const void*>(push_bulk_kernel<true, false>),
+        reinterpret_cast<const void*>(push_bulk_kernel<false, true>),
+        reinterpret_cast<const void*>(push_bulk_kernel<false, false>), reinterpret_cast<const void*>(slot_reduce_kernel),
+        reinterpret_cast<const void*>(fixed_finalize_kernel), reinterpret_cast<const void*>(barrier_kernel),
+        reinterpret_cast<const void*>(publish_kernel), reinterpret_cast<const void*>(gated_zero_kernel),
+        reinterpret_cast<const void*>(adam_kernel), reinterpret_cast<const void*>(init_shard_kernel)};
+    for (const void* f : fns) {
+        cudaFuncAttributes a;
+        const cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_init_shard(float* master, unsigned short* param, const float* src, std::int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     count_launch();

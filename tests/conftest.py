@@ -11,6 +11,8 @@ import pytest
 # block rank b's kernels queued behind it. 32 queues give every stream these
 # tests create its own. Must be set before the CUDA context exists.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# (the engine also force-loads its protocol kernels at context creation: a lazily loaded
+# kernel's first launch can wait for running work, i.e. for a peer's spinning barrier)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
