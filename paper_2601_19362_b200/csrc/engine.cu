@@ -25,7 +25,9 @@
 //                   ShardFabric::finalize_minibatch/take_grads :199-203, :144-148
 //   odc_adam_step   (no reference counterpart: the reference only accumulates)
 //
-// Ordering protocol (all device-side, sys scope):
+// Ordering protocol (all device-side, sys scope). The waits run in one small
+// gate kernel per stream and epoch (odc_ctx::gate), never inside the data-path
+// kernels, so a waiting rank holds no SMs a peer on the same GPU may need:
 //   * fetch of owner r's shard waits param_epoch[r] >= adams completed here;
 //   * every push into owner r waits drain_epoch[r] >= minibatches completed
 //     here: the owner has consumed what the previous minibatch left in its
@@ -47,6 +49,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "common.hpp"
@@ -112,6 +116,11 @@ struct odc_ctx {
     std::vector<char> touched;   // SLOT: [unit][owner] this client wrote its slot at the owner this minibatch
     std::int64_t off_marks = -1;  // SLOT: [unit][client] u64 "pushed in minibatch" marks (owner side)
     bool grads_pending = false;  // RED: the grad shards hold a finished minibatch not yet consumed
+    // Per stream: the parameter epoch / drain epoch whose gate kernel was already issued on it
+    // (stream order then covers every later fetch / push on that stream). The waits live in one
+    // tiny gate kernel instead of the data-path kernels, so a waiting rank never holds SMs that
+    // the rank it waits for needs (several ranks per GPU in one process).
+    std::unordered_map<cudaStream_t, std::pair<std::uint64_t, std::uint64_t>> gated;
     odc::AdamSeg* d_segs = nullptr;
     std::int64_t* d_seg_start = nullptr;
     std::int64_t adam_units = 0;
@@ -176,6 +185,21 @@ struct odc_ctx {
         cuda_ok(odc::launch_publish(drain_of(rank()), mb_epoch, s), "publish drain epoch");
         grads_pending = false;
     }
+    // Wait (device-side, one 32-thread block) until every owner's parameter epoch
+    // >= adams (param = true: fetch) or drain epoch >= mb_epoch (push), once per
+    // stream and epoch.
+    void gate(bool param, cudaStream_t s) {
+        const std::uint64_t need = param ? adams : mb_epoch;
+        auto it = gated.find(s);
+        if (it == gated.end()) it = gated.emplace(s, std::make_pair(~0ull, ~0ull)).first;
+        std::uint64_t& done = param ? it->second.first : it->second.second;
+        if (done != ~0ull && done >= need) return;
+        const unsigned long long* g[odc::kMaxSeg];
+        for (int r = 0; r < world(); ++r) g[r] = param ? epoch_of(r) : drain_of(r);
+        if (need > 0)  // epoch 0 is every flag's initial value
+            cuda_ok(odc::launch_gated_zero(nullptr, nullptr, 0, g, world(), need, err(), timeout_ns, s), "gate");
+        done = need;
+    }
     // rotation: rank r visits owners r+1, r+2, ..., r so that concurrent
     // fetches/pushes from all ranks spread over all owners' links
     int owner_at(int i) const { return (rank() + 1 + i) % world(); }
@@ -194,10 +218,7 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 void launch_fetch(const odc_ctx* c, const odc::SegTable& t, cudaStream_t s) {
     switch (c->cfg.fetch_engine) {
         case ODC_FETCH_LDG: cuda_ok(odc::launch_copy_segments(t, c->cfg.fetch_ctas, s), "fetch (ldg)"); return;
-        case ODC_FETCH_CE: {
-            const unsigned long long* gates[odc::kMaxSeg];
-            for (int i = 0; i < t.n; ++i) gates[i] = t.gate[i];
-            cuda_ok(odc::launch_gated_zero(nullptr, nullptr, 0, gates, t.n, t.need, t.err, t.timeout_ns, s), "gate");
+        case ODC_FETCH_CE: {  // the owners' epochs were awaited by the stream's gate kernel (odc_ctx::gate)
             for (int i = 0; i < t.n; ++i)
                 if (t.bytes[i] > 0)
                     cuda_ok(cudaMemcpyAsync(t.dst[i], t.src[i], static_cast<std::size_t>(t.bytes[i]),
@@ -453,9 +474,9 @@ odc_status odc_fetch(odc_ctx_t ch, int layer, void* dst_full, void* stream) {
             t.src[i] = reinterpret_cast<const char*>(c->param_of(r, u));
             t.dst[i] = static_cast<char*>(dst_full) + u.begin(r) * 2;
             t.bytes[i] = u.len(r) * 2;
-            t.gate[i] = c->epoch_of(r);
+            t.gate[i] = nullptr;
         }
-        t.need = c->adams;
+        c->gate(true, S(stream));
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
         launch_fetch(c, t, S(stream));
@@ -475,9 +496,9 @@ odc_status odc_fetch_master(odc_ctx_t ch, int layer, float* dst_full, void* stre
             t.src[i] = reinterpret_cast<const char*>(c->f32_of(r, u.off_master, u));
             t.dst[i] = reinterpret_cast<char*>(dst_full + u.begin(r));
             t.bytes[i] = u.len(r) * 4;
-            t.gate[i] = c->epoch_of(r);
+            t.gate[i] = nullptr;
         }
-        t.need = c->adams;
+        c->gate(true, S(stream));
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
         launch_fetch(c, t, S(stream));
@@ -505,14 +526,14 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
                 t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
                 t.dst[i] = c->slot_of(r, u, me);
                 t.elems[i] = u.len(r);
-                t.gate[i] = c->drain_of(r);
+                t.gate[i] = nullptr;
                 const bool first = !c->touched_at(layer, r);
                 t.assign[i] = first;
                 t.mark[i] = first ? c->mark_of(r, layer, me) : nullptr;
                 c->touched_at(layer, r) = 1;
             }
             t.mark_value = c->mb_epoch + 1;
-            t.need = c->mb_epoch;
+            c->gate(false, S(stream));
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
             cuda_ok(odc::launch_push_bulk(t, false, weight, 1.f, bf16, c->cfg.push_ctas, S(stream)), "push (slot)");
@@ -526,9 +547,9 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
                 t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
                 t.dst[i] = c->acc_of(r, u);
                 t.elems[i] = u.len(r);
-                t.gate[i] = c->drain_of(r);
+                t.gate[i] = nullptr;
             }
-            t.need = c->mb_epoch;  // the owner drained (converted + zeroed) the previous minibatch's sums
+            c->gate(false, S(stream));  // the owners drained (converted + zeroed) the previous minibatch's sums
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
             cuda_ok(odc::launch_push_bulk(t, true, weight, c->fixed_scale(), bf16, c->cfg.push_ctas, S(stream)),
@@ -553,9 +574,9 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
                 t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
                 t.dst[i] = c->f32_of(r, u.off_grad, u);
                 t.elems[i] = u.len(r);
-                t.gate[i] = c->drain_of(r);  // the owner consumed (zeroed) last minibatch's shard
+                t.gate[i] = nullptr;
             }
-            t.need = c->mb_epoch;
+            c->gate(false, S(stream));  // the owners consumed (zeroed) last minibatch's shard
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
             cuda_ok(odc::launch_push_bulk(t, false, weight, 1.f, bf16, c->cfg.push_ctas, S(stream)), "push (bulk)");
@@ -568,9 +589,9 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
             t.src[i] = static_cast<const char*>(grad_full) + u.begin(r) * (bf16 ? 2 : 4);
             t.dst[i] = c->f32_of(r, u.off_grad, u);
             t.elems[i] = u.len(r);
-            t.gate[i] = c->drain_of(r);
+            t.gate[i] = nullptr;
         }
-        t.need = c->mb_epoch;
+        c->gate(false, S(stream));
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
         cuda_ok(odc::launch_push_red(t, weight, bf16, c->cfg.push_ctas, S(stream)), "push");
@@ -596,11 +617,11 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
             const int me = c->rank();
             float* slot = c->slot_of(target, u, me);
             const bool first = !c->touched_at(layer, target);
-            if (first) {  // the slot still holds an older minibatch: zero it once the owner released it
+            c->gate(false, S(stream));
+            if (first) {  // the slot still holds an older minibatch: zero it (the owner released it)
                 float* p = slot;
                 std::int64_t cnt = u.len(target);
-                const unsigned long long* gate = c->drain_of(target);
-                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, &gate, 1, c->mb_epoch, c->err(), c->timeout_ns, S(stream)),
+                cuda_ok(odc::launch_gated_zero(&p, &cnt, 1, nullptr, 0, 0, c->err(), c->timeout_ns, S(stream)),
                         "slot zero");
                 c->touched_at(layer, target) = 1;
             }
@@ -622,8 +643,7 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
             t.src[0] = payload;
             t.dst[0] = c->acc_of(target, u) + offset;
             t.elems[0] = n;
-            t.gate[0] = c->drain_of(target);
-            t.need = c->mb_epoch;
+            c->gate(false, S(stream));
             t.err = c->err();
             t.timeout_ns = c->timeout_ns;
             cuda_ok(odc::launch_push_bulk(t, true, weight, c->fixed_scale(), false, 8, S(stream)), "push_slice (fixed)");
@@ -634,8 +654,7 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
         t.src[0] = payload;
         t.dst[0] = c->f32_of(target, u.off_grad, u) + offset;
         t.elems[0] = n;
-        t.gate[0] = c->drain_of(target);
-        t.need = c->mb_epoch;
+        c->gate(false, S(stream));
         t.err = c->err();
         t.timeout_ns = c->timeout_ns;
         cuda_ok(odc::launch_push_red(t, weight, false, 8, S(stream)), "push_slice");
