@@ -549,8 +549,9 @@ def run_sft(args):
                 "peak_kind": tkind, "frac": round(ach / tflops_peak, 4), "frac_vs_burst": round(ach / tflops_burst, 4),
                 "kernel": "odc::gemm::gemm2_kernel (tcgen05 cta_group::2, 256x256 tile per SM pair)",
                 "launches": gm["launches"], "ms_per_launch": round(gm["ms"] / gm["launches"], 4),
-                "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": ncu_traffic("gemm::gemm2_kernel"),
-                "traffic_source": "profiles/r01/ncu_traffic.json (dram read+write per launch, ncu --set full)"}
+                "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": ncu_traffic("gemm::gemm2_kernel")[0],
+                "traffic_source": f"{ncu_traffic('gemm::gemm2_kernel')[1]} (dram read+write per launch averaged over "
+                                  "the step's GEMM shapes, ncu --set full)"}
     pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
     # model FLOPs utilisation of the whole step: per sequence 6*P_nonembed*s (dense)
     # + 6*L*d*s^2 (causal attention, fwd+bwd) + 6*V*d*s (LM head); recompute is not counted
@@ -593,13 +594,17 @@ def run_sft(args):
 
 
 def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed ncu --set full capture (profiles/r01/ncu_traffic.json)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
-            return json.load(f)["kernels"][kernel]["dram_bytes_per_launch"]
-    except Exception:
-        return None
+    """(dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`,
+    source file) from the newest committed ncu --set full capture summary
+    (profiles/r02/ncu_traffic.json, else r01)."""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")
+        try:
+            with open(path) as f:
+                return json.load(f)["kernels"][kernel]["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
 
 
 def comm_rates(eng, M, rank, world, dev, reps=10):

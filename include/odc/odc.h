@@ -92,6 +92,11 @@ typedef struct odc_fabric* odc_fabric_t;
 
 /* ShardState(ranks, elems) :38-48 — ParamError if ranks < 1 or elems < 1 */
 odc_status odc_fabric_create(int ranks, int64_t elems, odc_dtype dtype, int device, odc_fabric_t* out);
+/* single-process multi-GPU: simulated rank r's shards, accumulator and server
+ * slots on devices[r % ndev]; staging and kernels on devices[0], which reads
+ * and writes the others' HBM through peer access over NVLink */
+odc_status odc_fabric_create_multi(int ranks, int64_t elems, odc_dtype dtype, const int* devices, int ndev,
+                                   odc_fabric_t* out);
 odc_status odc_fabric_destroy(odc_fabric_t f);
 /* scatter_accumulate strategy: ODC_PUSH_SLOT (default) = the reference's
  * staged protocol (stage into the (owner, client) slot, the owner consumes the

@@ -46,6 +46,24 @@ inline int fabric_device() {
     const char* d = std::getenv("ODC_DEVICE");
     return d ? std::atoi(d) : 0;
 }
+// ODC_DEVICES="0,1,2,3": single-process multi-GPU mode (simulated rank r on the
+// r % n-th listed GPU); otherwise every rank on ODC_DEVICE (default 0)
+inline std::vector<int> fabric_devices() {
+    std::vector<int> out;
+    if (const char* d = std::getenv("ODC_DEVICES")) {
+        std::string s(d);
+        std::size_t pos = 0;
+        while (pos < s.size()) {
+            const std::size_t comma = s.find(',', pos);
+            const std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+            if (!tok.empty()) out.push_back(std::atoi(tok.c_str()));
+            if (comma == std::string::npos) break;
+            pos = comma + 1;
+        }
+    }
+    if (out.empty()) out.push_back(fabric_device());
+    return out;
+}
 }  // namespace detail
 
 // One gradient slice addressed to the owner of that slice.
@@ -64,7 +82,9 @@ public:
     ShardState(int ranks, std::int64_t elems) : ranks_(ranks), elems_(elems) {
         if (ranks < 1 || elems < 1) throw ParamError("need ranks >= 1 and elems >= 1");
         block_ = (elems + ranks - 1) / ranks;
-        detail::check(odc_fabric_create(ranks, elems, detail::dtype_of<T>(), detail::fabric_device(), &f_));
+        const std::vector<int> devs = detail::fabric_devices();
+        detail::check(odc_fabric_create_multi(ranks, elems, detail::dtype_of<T>(), devs.data(),
+                                              static_cast<int>(devs.size()), &f_));
     }
     ~ShardState() { odc_fabric_destroy(f_); }
     ShardState(const ShardState&) = delete;

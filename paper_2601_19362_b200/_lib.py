@@ -42,6 +42,7 @@ SIGNATURES = {
     "odc_kernel_launches": (C.c_uint64, []),
     "odc_shard_range": (C.c_int, [i64, C.c_int, C.c_int, i64p, i64p]),
     "odc_fabric_create": (C.c_int, [C.c_int, i64, C.c_int, C.c_int, C.POINTER(vp)]),
+    "odc_fabric_create_multi": (C.c_int, [C.c_int, i64, C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]),
     "odc_fabric_destroy": (C.c_int, [vp]),
     "odc_fabric_set_push_mode": (C.c_int, [vp, C.c_int]),
     "odc_fabric_set_params": (C.c_int, [vp, C.c_char_p, vp, i64]),

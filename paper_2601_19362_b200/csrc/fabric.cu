@@ -15,6 +15,7 @@
 // so float/double results are bit-identical to the reference, not just close.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <string>
@@ -54,16 +55,22 @@ struct odc_fabric {
     odc_push_mode mode = ODC_PUSH_SLOT;
     cudaStream_t stream = nullptr;
 
-    // one allocation per shard set; rank r's shard at base + r*stride + pad_r
+    // Single-process multi-GPU mode (odc_fabric_create_multi): simulated rank r's
+    // shards, gradient accumulator and server-side slots live on rank_dev[r];
+    // the host staging / output buffers and every kernel live on `device`, which
+    // reaches the other GPUs' memory through peer access over NVLink.
+    std::vector<int> rank_dev;
+
+    // one allocation per (shard set, device); rank r's shard at base_of_its_device + k*stride + pad_r
     struct ShardSet {
-        char* base = nullptr;
+        std::vector<char*> bases;  // allocations to free
         std::vector<char*> ptr;
     };
     std::int64_t stride_bytes = 0;
     std::map<std::string, ShardSet> params;
     ShardSet grads;
 
-    char* slots = nullptr;  // [server][client] x block elements
+    std::vector<char*> slots;  // per server s: [client] x block elements, on rank_dev[s]
     std::vector<unsigned char> occ;
     std::vector<std::int64_t> slot_off, slot_len;
     std::vector<std::uint64_t> slot_w;  // weight bits
@@ -77,20 +84,43 @@ struct odc_fabric {
         return std::min<std::int64_t>(elems, static_cast<std::int64_t>(r + 1) * block) - begin(r);
     }
     char* slot_ptr(int s, int c) const {
-        return slots + (static_cast<std::int64_t>(s) * ranks + c) * block * static_cast<std::int64_t>(es);
+        return slots[static_cast<std::size_t>(s)] + static_cast<std::int64_t>(c) * block * static_cast<std::int64_t>(es);
     }
     std::size_t sidx(int s, int c) const { return static_cast<std::size_t>(s) * ranks + c; }
 
     ShardSet alloc_set() {
         ShardSet s;
-        const std::int64_t total = stride_bytes * ranks;
-        cuda_ok(cudaMalloc(&s.base, static_cast<std::size_t>(total)), "cudaMalloc shards");
-        cuda_ok(cudaMemsetAsync(s.base, 0, static_cast<std::size_t>(total), stream), "memset shards");
-        for (int r = 0; r < ranks; ++r) {
-            const std::int64_t pad = (begin(r) * static_cast<std::int64_t>(es)) % 16;
-            s.ptr.push_back(s.base + r * stride_bytes + pad);
+        s.ptr.assign(static_cast<std::size_t>(ranks), nullptr);
+        std::vector<int> devs(rank_dev);
+        std::sort(devs.begin(), devs.end());
+        devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+        for (int d : devs) {  // the ranks of device d share one allocation there
+            std::vector<int> rs;
+            for (int r = 0; r < ranks; ++r)
+                if (rank_dev[static_cast<std::size_t>(r)] == d) rs.push_back(r);
+            char* base = nullptr;
+            const std::int64_t total = stride_bytes * static_cast<std::int64_t>(rs.size());
+            cuda_ok(cudaSetDevice(d), "cudaSetDevice");
+            cuda_ok(cudaMalloc(&base, static_cast<std::size_t>(total)), "cudaMalloc shards");
+            cuda_ok(cudaMemset(base, 0, static_cast<std::size_t>(total)), "memset shards");
+            s.bases.push_back(base);
+            for (std::size_t k = 0; k < rs.size(); ++k) {
+                const int r = rs[k];
+                const std::int64_t pad = (begin(r) * static_cast<std::int64_t>(es)) % 16;
+                s.ptr[static_cast<std::size_t>(r)] = base + static_cast<std::int64_t>(k) * stride_bytes + pad;
+            }
         }
+        set_device();
         return s;
+    }
+    // zero every rank's accumulator (a kernel on `device`: the shards may be on peer GPUs)
+    void zero_set(ShardSet& set) {
+        for (int r = 0; r < ranks; ++r) {
+            float* p = reinterpret_cast<float*>(set.ptr[static_cast<std::size_t>(r)]);
+            std::int64_t n = len(r) * static_cast<std::int64_t>(es) / 4;  // es is 4 or 8: whole fp32 words
+            if (n > 0)
+                cuda_ok(odc::launch_gated_zero(&p, &n, 1, nullptr, 0, 0, nullptr, 0, stream), "zero grads");
+        }
     }
 
     void set_device() const { cuda_ok(cudaSetDevice(device), "cudaSetDevice"); }
@@ -184,7 +214,7 @@ struct odc_fabric {
             8, "collect grads");
         cuda_ok(cudaMemcpyAsync(host_out, out, static_cast<std::size_t>(elems) * es, cudaMemcpyDeviceToHost, stream),
                 "D2H grads");
-        cuda_ok(cudaMemsetAsync(grads.base, 0, static_cast<std::size_t>(stride_bytes * ranks), stream), "zero grads");
+        zero_set(grads);
         cuda_ok(cudaStreamSynchronize(stream), "sync");
     }
 };
@@ -201,10 +231,12 @@ void check_rank(const odc_fabric* f, int r, const char* what) {
 
 extern "C" {
 
-odc_status odc_fabric_create(int ranks, std::int64_t elems, odc_dtype dtype, int device, odc_fabric_t* out) {
+odc_status odc_fabric_create_multi(int ranks, std::int64_t elems, odc_dtype dtype, const int* devices, int ndev,
+                                   odc_fabric_t* out) {
     return odc::guard([&] {
         if (ranks < 1 || elems < 1) throw ParamError("need ranks >= 1 and elems >= 1");
         if (ranks > 4096) throw ParamError("too many ranks");
+        if (!devices || ndev < 1) throw ParamError("need at least one device");
         auto* f = new odc_fabric();
         try {
             f->ranks = ranks;
@@ -212,13 +244,29 @@ odc_status odc_fabric_create(int ranks, std::int64_t elems, odc_dtype dtype, int
             f->block = (elems + ranks - 1) / ranks;
             f->dt = dtype;
             f->es = dtype_size(dtype);
-            f->device = device;
+            f->device = devices[0];
+            for (int r = 0; r < ranks; ++r) f->rank_dev.push_back(devices[r % ndev]);
             f->set_device();
+            for (int i = 0; i < ndev; ++i) {  // the primary device's kernels reach every shard
+                if (devices[i] == f->device) continue;
+                int ok = 0;
+                cuda_ok(cudaDeviceCanAccessPeer(&ok, f->device, devices[i]), "cudaDeviceCanAccessPeer");
+                if (!ok) throw ParamError("no peer access from the primary device to device " + std::to_string(devices[i]));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(devices[i], 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else cuda_ok(e, "cudaDeviceEnablePeerAccess");
+            }
             cuda_ok(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking), "stream");
             f->stride_bytes = ((f->block * static_cast<std::int64_t>(f->es) + 16 + 255) / 256) * 256;
             f->grads = f->alloc_set();
-            const std::int64_t slot_bytes = static_cast<std::int64_t>(ranks) * ranks * f->block * f->es;
-            cuda_ok(cudaMalloc(&f->slots, static_cast<std::size_t>(std::max<std::int64_t>(slot_bytes, 16))), "slots");
+            const std::int64_t slot_bytes = static_cast<std::int64_t>(ranks) * f->block * f->es;
+            for (int sv = 0; sv < ranks; ++sv) {  // server sv's slots live with its shard
+                char* p = nullptr;
+                cuda_ok(cudaSetDevice(f->rank_dev[static_cast<std::size_t>(sv)]), "cudaSetDevice");
+                cuda_ok(cudaMalloc(&p, static_cast<std::size_t>(std::max<std::int64_t>(slot_bytes, 16))), "slots");
+                f->slots.push_back(p);
+            }
+            f->set_device();
             cuda_ok(cudaMalloc(&f->stage, static_cast<std::size_t>(elems) * f->es + 16), "stage");
             cuda_ok(cudaMalloc(&f->out, static_cast<std::size_t>(elems) * f->es + 16), "out");
             const std::size_t nn = static_cast<std::size_t>(ranks) * ranks;
@@ -237,13 +285,18 @@ odc_status odc_fabric_create(int ranks, std::int64_t elems, odc_dtype dtype, int
     });
 }
 
+odc_status odc_fabric_create(int ranks, std::int64_t elems, odc_dtype dtype, int device, odc_fabric_t* out) {
+    return odc_fabric_create_multi(ranks, elems, dtype, &device, 1, out);
+}
+
 odc_status odc_fabric_destroy(odc_fabric_t f) {
     if (!f) return ODC_OK;
     cudaSetDevice(f->device);
     if (f->stream) cudaStreamSynchronize(f->stream);
-    for (auto& kv : f->params) cudaFree(kv.second.base);
-    cudaFree(f->grads.base);
-    cudaFree(f->slots);
+    for (auto& kv : f->params)
+        for (char* b : kv.second.bases) cudaFree(b);
+    for (char* b : f->grads.bases) cudaFree(b);
+    for (char* b : f->slots) cudaFree(b);
     cudaFree(f->stage);
     cudaFree(f->out);
     if (f->stream) cudaStreamDestroy(f->stream);

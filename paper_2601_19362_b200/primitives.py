@@ -114,14 +114,19 @@ class ShardFabric:
     push_mode: "slot" (default) = the reference's staged protocol, bit-exact
     in every dtype; "red" = remote red.add straight into owner shards."""
 
-    def __init__(self, ranks: int, elems: int, dtype=np.int64, device: int = 0, push_mode: str = "slot"):
+    def __init__(self, ranks: int, elems: int, dtype=np.int64, device: int = 0, push_mode: str = "slot",
+                 devices=None):
+        """devices: single-process multi-GPU mode — simulated rank r's shards
+        and slots on devices[r % len(devices)], kernels on devices[0]."""
         self.dtype = np.dtype(dtype)
         if self.dtype not in _DT:
             from .errors import ParamError
 
             raise ParamError("ShardFabric dtype must be int64, float64 or float32")
         h = C.c_void_p()
-        check(lib().odc_fabric_create(ranks, elems, _DT[self.dtype], device, C.byref(h)))
+        devs = list(devices) if devices else [device]
+        arr = (C.c_int * len(devs))(*devs)
+        check(lib().odc_fabric_create_multi(ranks, elems, _DT[self.dtype], arr, len(devs), C.byref(h)))
         self.h = h
         self.ranks, self.elems = ranks, elems
         self.block = (elems + ranks - 1) // ranks

@@ -136,3 +136,21 @@ def test_fabric_more_ranks_than_one_copy_table(ranks):
         f.scatter_accumulate(c, g, w)
         o.scatter_accumulate(c, g, w)
     assert np.array_equal(np.concatenate(f.finalize_minibatch()), np.concatenate(o.finalize_minibatch()))
+
+
+@pytest.mark.parametrize("dt", [np.int64, np.float32])
+def test_fabric_single_process_multi_gpu(dt):
+    """odc_fabric_create_multi: simulated ranks spread over every GPU of the box
+    (rank r on GPU r % n; on a one-GPU box the ranks still get per-device
+    allocations) — the reference's fixture scripts stay bit-exact."""
+    import torch
+
+    devs = list(range(torch.cuda.device_count())) * 2
+    for case in golden("fabric_scripts.json")[:40]:
+        if np.dtype(case["dtype"]) != np.dtype(dt):
+            continue
+        f = ShardFabric(case["ranks"], case["elems"], dt, devices=devs[:max(1, min(len(devs), case["ranks"]))])
+        for c, g, w in case["pushes"]:
+            f.scatter_accumulate(c, np.asarray(g, dt), w)
+        assert np.array_equal(np.concatenate(f.finalize_minibatch()), np.asarray(case["expected"], dt))
+        assert not np.concatenate(f.finalize_minibatch()).any()
