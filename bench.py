@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="odc", choices=["odc", "reference"])
-    ap.add_argument("--workload", default="sft", choices=["sft", "odc_minibatch_comm"])
+    ap.add_argument("--workload", default="sft", choices=["sft", "odc_minibatch_comm", "config0"],
+                    help="config0 = BASELINE configs[0]: the small transformer at world 2 on the survey's 16 lengths")
     ap.add_argument("--no-fsdp", action="store_true", help="skip the same-box NCCL FSDP comparison arm")
     ap.add_argument("--trace", default="", help="write a Chrome trace (reference schema) of one extra ODC step")
     ap.add_argument("--cost", default="b200", choices=["b200", "flops"],
@@ -726,8 +727,194 @@ def cpu_step_baseline(args, shape, world, beta, steps, budget_s=30.0):
                        f"1 scatter_accumulate per unit per microbatch, finalize per unit, + plan()); {thr} host threads")}
 
 
+# ----------------------------------------------------------------- configs[0]
+CONFIG0_LENS = [451, 131, 1078, 28, 2048, 77, 27, 63, 76, 119, 89, 601, 435, 90, 712, 264]  # SURVEY 8(c) fixture
+
+
+def config0_shape():
+    """configs[0]: small transformer, d=256, 4 layers, ffn 1024, vocab 1024, tied
+    (2 heads of 128: the tcgen05 attention serves head_dim 128)."""
+    from paper_2601_19362_b200.shapes import Shape
+
+    return Shape("config0", 256, 1024, 4, 2, 2, 1024, True, True)
+
+
+def cpu_decoder_loss(shape, units, batch):
+    """The decoder of the SFT worker in plain torch fp32 (CPU): RMSNorm, qkv
+    (+bias), RoPE, causal SDPA per sequence (GQA), o-proj, SwiGLU MLP, tied LM
+    head + CE. Gradients flow into `units` (leaf tensors)."""
+    import torch
+    import torch.nn.functional as TF
+
+    from paper_2601_19362_b200 import worker as W
+
+    s = shape
+    E = W.views(units[0], W.embed_layout(s))
+    T = batch.tokens
+    h = E["emb"][batch.ids]
+    cos, sin = W.rope_tables(batch.positions, s.head_dim)
+    cu = batch.cu_seqlens.tolist()
+    hd, H, KV = s.head_dim, s.heads, s.kv_heads
+
+    def rms(x, w):
+        return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + W.EPS) * w
+
+    def rope(x):
+        hh = x.shape[-1] // 2
+        x1, x2 = x[..., :hh], x[..., hh:]
+        return torch.cat([x1 * cos[:, None] - x2 * sin[:, None], x2 * cos[:, None] + x1 * sin[:, None]], -1)
+
+    for l in range(1, s.layers + 1):
+        P = W.views(units[l], W.layer_layout(s))
+        qkv = rms(h, P["ln1"]) @ P["qkv_w"].t() + (P["qkv_b"] if s.qkv_bias else 0.0)
+        q = rope(qkv[:, :H * hd].view(T, H, hd))
+        k = rope(qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd))
+        v = qkv[:, (H + KV) * hd:].reshape(T, KV, hd)
+        outs = []
+        for i in range(len(cu) - 1):
+            qs, ks, vs = (t[cu[i]:cu[i + 1]].transpose(0, 1) for t in (q, k, v))
+            outs.append(TF.scaled_dot_product_attention(qs[None], ks.repeat_interleave(H // KV, 0)[None],
+                                                        vs.repeat_interleave(H // KV, 0)[None],
+                                                        is_causal=True)[0].transpose(0, 1))
+        h = h + torch.cat(outs, 0).reshape(T, H * hd) @ P["o_w"].t()
+        gu = rms(h, P["ln2"]) @ P["gu_w"].t()
+        h = h + (TF.silu(gu[:, :s.ffn]) * gu[:, s.ffn:]) @ P["down_w"].t()
+    logits = rms(h, E["norm"]) @ (E["emb"] if s.tied else E["head"]).t()
+    return TF.cross_entropy(logits, batch.labels, ignore_index=-100)
+
+
+def run_config0(args, reference: bool):
+    """BASELINE configs[0] — the reference's CPU-runnable case: one ODC SFT
+    step of the small transformer at world_size 2 on the survey's 16 fixed
+    lengths (LB-Mini, minibatch 8 per rank, budget 2,048 tokens, alpha 1, beta 0:
+    rank 0 [[4]], rank 1 [[2],[3,6,12,14],[0,1,...]]).
+      GPU arm: both ranks in one process on cuda:0 (OdcEngine.local_group: the
+        world-2 fetch / push / barrier protocol, FIXED push, AdamW), tcgen05
+        worker; a step = both ranks' queues + barrier + AdamW.
+      reference arm: the same step on host cores — the model in plain torch fp32
+        (cpu_decoder_loss, every core) and the data path through the reference's
+        ShardFabric<float> of 2 simulated ranks per unit (oracle/_ref); plan and
+        lengths from the reference's plan()."""
+    import torch
+
+    from paper_2601_19362_b200 import worker as W
+
+    s = config0_shape()
+    sizes = W.unit_sizes(s)
+    lens = CONFIG0_LENS
+    tokens = sum(lens)
+    cfg = {"workload": "config0", "model": "config0 (d256 L4 ffn1024 V1024, 2 heads x 128)", "world": 2,
+           "plan": "lb-mini minibs 8 budget 2048 alpha 1 beta 0", "lengths": "SURVEY 8(c) fixture (16 samples)"}
+    if reference:
+        from oracle import refbind as R
+
+        js = json.loads(R.plan_json("lb-mini", lens, 2, 8, 2048, 1.0, 0.0, 1))
+        plan = [[mb["sample_ids"] for mb in dev] for dev in js["steps"][0]["per_device"]]
+        torch.set_num_threads(len(os.sched_getaffinity(0)))
+        gen = torch.Generator().manual_seed(0)
+        units = [W.init_unit(s, u, gen, "cpu").requires_grad_(True) for u in range(len(sizes))]
+        timer = RefStepTimer(2, sizes, min(len(sizes), len(os.sched_getaffinity(0))))
+
+        def step():
+            t0 = time.perf_counter()
+            for dev in plan:
+                for mb in dev:
+                    b = W.make_batch(lens, mb, s.vocab, "cpu")
+                    loss = cpu_decoder_loss(s, units, b) * (sum(lens[i] for i in mb) / tokens)
+                    loss.backward()
+            for u in units:
+                u.grad = None
+            return time.perf_counter() - t0 + timer.run(plan)
+
+        for _ in range(args.warmup):
+            step()
+        secs = [step() for _ in range(args.steps)]
+        timer.close()
+        tps = tokens * len(secs) / sum(secs)
+        line = {"metric": METRIC, "impl": "reference", "value": round(tps, 1), "unit": "tokens/s", "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sum(secs) / len(secs) * 1e3, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": cfg,
+                "cpu_baseline": {"value": round(tps, 1), "unit": "tokens/s", "cores": torch.get_num_threads(),
+                                 "kind": "port", "sample": "configs[0] step: torch fp32 model on CPU + reference "
+                                                           "ShardFabric<float> (2 ranks) per unit, every microbatch"},
+                "e2e": {"value": round(tps, 1), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    from paper_2601_19362_b200 import _lib
+    from paper_2601_19362_b200 import partition as P
+    from paper_2601_19362_b200.engine import OdcEngine
+
+    dev = torch.device("cuda", 0)
+    plan = P.plan_flat("lb-mini", lens, 2, 8, 2048, P.CostModel(1.0, 0.0, 1))[0]
+    engs = OdcEngine.local_group(sizes, 2, [0], push_mode="fixed")
+    gen = torch.Generator(device=dev).manual_seed(0)
+    for u in range(len(sizes)):
+        full = W.init_unit(s, u, gen, dev)
+        for e in engs:
+            e.set_params(u, full)
+    streams = [torch.cuda.Stream(device=dev) for _ in engs]
+    workers = []
+    for e, st in zip(engs, streams):
+        with torch.cuda.stream(st):
+            workers.append(W.Worker(s, W.OdcComm(e), dev, ce_chunk=2048))
+    torch.cuda.synchronize()
+
+    def step(host_batches: bool, pre=None):
+        losses = []
+        for r, (wk, st) in enumerate(zip(workers, streams)):
+            with torch.cuda.stream(st):
+                for j, mb in enumerate(plan[r]):
+                    b = pre[r][j] if pre else W.make_batch(lens, mb, s.vocab, dev, heads=s.heads, kv_heads=s.kv_heads)
+                    losses.append(wk.microbatch(b, sum(lens[i] for i in mb) / tokens))
+        for wk, st in zip(workers, streams):
+            with torch.cuda.stream(st):
+                wk.minibatch_end(lr=1e-5)
+        return losses
+
+    def timed(host_batches):
+        pre = None if host_batches else [[W.make_batch(lens, mb, s.vocab, dev, heads=s.heads, kv_heads=s.kv_heads)
+                                          for mb in plan[r]] for r in range(2)]
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in streams]
+        for (a, _), st in zip(evs, streams):
+            a.record(st)
+        n0 = _lib.kernel_launches()
+        for _ in range(args.steps):
+            losses = step(host_batches, pre)
+            if host_batches:
+                float(sum(x.item() for x in losses))  # D2H of the step's loss
+        for (_, b), st in zip(evs, streams):
+            b.record(st)
+        torch.cuda.synchronize()
+        ms = max(a.elapsed_time(b) for a, b in evs)
+        return ms, _lib.kernel_launches() - n0
+
+    for _ in range(args.warmup):
+        step(True)
+    torch.cuda.synchronize()
+    for e in engs:
+        e.check()
+    ms, launches = timed(False)
+    ms_e2e, _ = timed(True)
+    for e in engs:
+        e.check()
+    line = {"metric": METRIC, "value": round(tokens * args.steps / (ms / 1e3), 1), "unit": "tokens/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": cfg, "note": "two ODC ranks in one process on one GPU (world-2 protocol, FIXED push)",
+            "e2e": {"value": round(tokens * args.steps / (ms_e2e / 1e3), 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(16 * tokens + 8 * 34), "d2h_bytes_per_step": 4 * len(plan[0] + plan[1])},
+            "gpu_launches": int(launches)}
+    print(json.dumps(line), flush=True)
+    for e in engs:
+        e.close()
+
+
 def main():
     args = parse()
+    if args.workload == "config0":
+        return run_config0(args, reference=args.impl == "reference")
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "sft":

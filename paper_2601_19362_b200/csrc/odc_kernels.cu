@@ -208,7 +208,7 @@ cudaError_t launch_copy_segments(const SegTable& t, int ctas, cudaStream_t s) {
 // a resident GEMM/attention CTA reached only 340 GB/s and did not change the
 // SFT step (profiles/r01/p2p_n2_smallsmem.md), so the big ring stays.
 constexpr int kTmaChunk = 32768;
-constexpr int kTmaStages = 4;
+constexpr int kTmaStages = 5;  // 4 peer loads in flight + 1 stage whose store to local HBM is still reading smem
 constexpr int kTmaThreads = 64;
 constexpr int kTmaSmem = kTmaChunk * kTmaStages;
 
@@ -315,14 +315,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) fetch_tma_kernel(SegTable t) {
             "l"(t.src[seg[st]] + off[st]), "r"(nbytes[st]), "r"(b)
             : "memory");
     };
-    int inflight = 0;
-    for (int st = 0; st < kTmaStages; ++st) {
+    // Stages are consumed in load-issue order (a FIFO of stage ids). A consumed
+    // stage is stored to local HBM and refilled only one iteration later, after
+    // `wait_group.read 1` (every store but the newest has read its smem): the
+    // peer loads never wait for the store that was just issued.
+    int fifo[kTmaStages];
+    int head = 0, count = 0;
+    for (int st = 0; st < kTmaStages - 1; ++st) {
         if (!jobs.next(seg[st], off[st], nbytes[st])) break;
         load(st);
-        ++inflight;
+        fifo[(head + count++) % kTmaStages] = st;
     }
-    for (int j = 0; inflight > 0; ++j) {
-        const int st = j % kTmaStages;
+    int spare = kTmaStages - 1;  // the stage kept free for the store in flight
+    int stored = -1;             // stage whose store was issued last iteration (refill candidate)
+    while (count > 0) {
+        const int st = fifo[head];
+        head = (head + 1) % kTmaStages;
+        --count;
         asm volatile(
             "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
                 smem_u32(&bar[st])),
@@ -333,12 +342,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) fetch_tma_kernel(SegTable t) {
                      "r"(smem_u32(smem + st * kTmaChunk)), "r"(nbytes[st])
                      : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        --inflight;
-        if (jobs.next(seg[st], off[st], nbytes[st])) {
-            // the stage's smem may be refilled once the store has read it
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            load(st);
-            ++inflight;
+        // refill: the spare stage (never used yet) first, then the stage stored one iteration ago
+        int refill = spare;
+        if (refill < 0) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            refill = stored;
+        }
+        spare = -1;
+        stored = st;
+        if (refill >= 0 && jobs.next(seg[refill], off[refill], nbytes[refill])) {
+            load(refill);
+            fifo[(head + count++) % kTmaStages] = refill;
         }
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

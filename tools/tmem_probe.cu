@@ -75,7 +75,9 @@ __host__ __device__ constexpr unsigned instr(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((static_cast<unsigned>(n) >> 3) << 17) | ((128u >> 4) << 24);
 }
 
-// mode 0: SS N=128, 1: SS N=256, 2: TS N=128 (A from TMEM cols [256, 320))
+// mode 0: SS N=128, 1: SS N=256, 2: TS N=128 (A from TMEM cols [256, 320));
+// modes 3-5: the same three, alternating between two independent accumulators
+// (D at cols 0 and 128 for N=128, 0 and 256 for N=256) instruction by instruction
 __global__ void mma_probe(int iters, int mode, unsigned long long* cyc) {
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -98,7 +100,9 @@ __global__ void mma_probe(int iters, int mode, unsigned long long* cyc) {
     const unsigned t = tbase;
     if (threadIdx.x == 0) {
         const unsigned a = su32(smem), b = su32(smem + 32768);
-        const int n = mode == 1 ? 256 : 128;
+        const int base_mode = mode % 3;
+        const bool alt = mode >= 3;
+        const int n = base_mode == 1 ? 256 : 128;
         const unsigned id = instr(n);
         const unsigned long long c0 = clock64();
         for (int i = 0; i < iters; ++i) {
@@ -107,17 +111,18 @@ __global__ void mma_probe(int iters, int mode, unsigned long long* cyc) {
                 const unsigned off = (kk >> 2) * 16384 + (kk & 3) * 32;
                 const std::uint64_t bd = sdesc(b + off, 16, 1024);
                 const unsigned acc = (i | kk) ? 1u : 0u;
-                if (mode == 2) {
+                const unsigned d = t + ((alt && (kk & 1)) ? static_cast<unsigned>(n) : 0u);
+                if (base_mode == 2) {
                     asm volatile(
                         "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(t),
-                        "r"(t + 256 + kk * 8), "l"(bd), "r"(id), "r"(acc)
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
+                        "r"(t + 384 + kk * 8), "l"(bd), "r"(id), "r"(acc)
                         : "memory");
                 } else {
                     const std::uint64_t ad = sdesc(a + off, 16, 1024);
                     asm volatile(
                         "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(t),
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
                         "l"(ad), "l"(bd), "r"(id), "r"(acc)
                         : "memory");
                 }
@@ -156,14 +161,16 @@ int main() {
                double(h[0]) / iters, bytes / double(h[0]), cudaGetErrorString(cudaGetLastError()));
     }
     cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    const char* names[] = {"SS M128 N128 K16", "SS M128 N256 K16", "TS M128 N128 K16"};
-    for (int mode = 0; mode < 3; ++mode) {
+    const char* names[] = {"SS M128 N128 K16", "SS M128 N256 K16", "TS M128 N128 K16",
+                           "SS M128 N128 K16, 2 accumulators alternating", "SS M128 N256 K16, 2 accumulators alternating",
+                           "TS M128 N128 K16, 2 accumulators alternating"};
+    for (int mode = 0; mode < 6; ++mode) {
         const int it = 2000;
         mma_probe<<<148, 128, 100 * 1024>>>(it, mode, cyc);
         cudaDeviceSynchronize();
         unsigned long long h[148];
         cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost);
-        const double n = mode == 1 ? 256 : 128;
+        const double n = mode % 3 == 1 ? 256 : 128;
         const double per = double(h[0]) / (it * 8.0);
         printf("%s: %.1f cycles/instr, %.0f MAC/clk/SM (err %s)\n", names[mode], per, 128.0 * n * 16 / per,
                cudaGetErrorString(cudaGetLastError()));
