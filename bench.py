@@ -584,9 +584,10 @@ def run_sft(args):
                              "analytic_bubble_fsdp_lbmicro": round(pred[2], 4)} if fs else None),
                 "roofline": roof, "mfu": mfu, "fetch_push": comm, "clocks": clk.summary(),
                 "e2e": ({"value": round(e2e["tps"], 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / args.steps),
-                         "d2h_bytes_per_step": 4, "loss": e2e["loss"],
+                         "d2h_bytes_per_step": 4, "loss_rank0": e2e["loss"],
                          "note": "token ids/labels/positions built on host per microbatch, staged in pinned host memory and copied H2D (async) inside the "
-                                 "timed region; loss read back D2H every step"} if e2e else None),
+                                 "timed region; loss read back D2H every step (loss_rank0 = rank 0's token-weighted share of the "
+                                 "step's mean loss: ~ln(V) x its token fraction)"} if e2e else None),
                 "cpu_baseline": cpu, "gpu_launches": res["launches"]}
         print(json.dumps(line), flush=True)
     eng.close()
@@ -628,12 +629,30 @@ def comm_rates(eng, M, rank, world, dev, reps=10):
         if world > 1:
             dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms, _, _, _ = rank_timings(a.elapsed_time(b) / reps, 0.0, 0, device=dev)
+        if name == "push" and eng.push_mode == "slot":
+            # SLOT: a unit's first push of the minibatch is the store into the owners' slots; time
+            # those (the untimed minibatch_end between them releases the slots)
+            tot = 0.0
+            for _ in range(reps):
+                eng.minibatch_end()
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                tot += a.elapsed_time(b)
+            ms, _, _, _ = rank_timings(tot / reps, 0.0, 0, device=dev)
+            eng.minibatch_end()
+            torch.cuda.synchronize()
+        else:
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms, _, _, _ = rank_timings(a.elapsed_time(b) / reps, 0.0, 0, device=dev)
         block = (M + world - 1) // world
         wire = 8 if eng.push_mode == "fixed" else 4  # FIXED push moves int64 fixed-point values
         if world > 1:

@@ -464,10 +464,8 @@ class Worker:
             tr = self.tracer.span("bwd", l, cur, False) if self.tracer else None
             x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = self._restore(P, saved[l - 1], b)
             # MLP block
-            dm = G.linear_dgrad(dh, P["down_w"])
+            dgu = G.down_dgrad_swiglu_bwd(dh, P["down_w"], gu, s.ffn)  # SwiGLU bwd in the dgrad epilogue
             G.linear_wgrad(dh, m, out=Gv["down_w"])
-            dgu = F.swiglu_bwd(dm, gu, s.ffn)
-            del dm
             dbn = G.linear_dgrad(dgu, P["gu_w"])
             G.linear_wgrad(dgu, bn, out=Gv["gu_w"])
             del dgu

@@ -72,3 +72,24 @@ def test_gate_up_swiglu_fused_matches_unfused(T, d, ffn):
     assert torch.equal(m, F.swiglu_fwd(gu_ref, ffn))
     g, u = gu_ref.float()[:, :ffn], gu_ref.float()[:, ffn:]
     torch.testing.assert_close(m.float(), torch.nn.functional.silu(g) * u, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("T,d,ffn", [(100, 256, 512), (1000, 1536, 8960), (4097, 512, 1024), (32768, 1536, 8960),
+                                     (600, 256, 640)])
+def test_down_dgrad_swiglu_bwd_fused_matches_unfused(T, d, ffn):
+    """SwiGLU backward fused into the down-proj dgrad epilogue: dgu
+    bit-identical to the plain dgrad (dm stored as bf16) followed by the
+    standalone swiglu_bwd kernel (T < 256 or ffn % 256 != 0 run that pair)."""
+    from paper_2601_19362_b200 import fused as F
+
+    dh = _r(T, d)
+    w_down = (torch.randn(d, ffn, device=DEV) * 0.05).to(torch.bfloat16)
+    gu = _r(T, 2 * ffn)
+    dgu = G.down_dgrad_swiglu_bwd(dh, w_down, gu, ffn)
+    dm = G.linear_dgrad(dh, w_down)
+    assert torch.equal(dgu, F.swiglu_bwd(dm, gu, ffn))
+    g, u = gu.float()[:, :ffn], gu.float()[:, ffn:]
+    sg = torch.sigmoid(g)
+    dmf = dm.float()
+    want = torch.cat([dmf * u * sg * (1 + g * (1 - sg)), dmf * g * sg], 1)
+    torch.testing.assert_close(dgu.float(), want, rtol=3e-2, atol=3e-2)
