@@ -268,6 +268,14 @@ odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void*
                         const float* lse, void* dq, void* dk, void* dv, void* workspace, const void* items,
                         int n_items, int64_t T, int H, int KV, int head_dim, float scale, void* stream);
 
+/* The backward straight to the packed qkv gradient: dqkv [T][(H+2KV)*128] bf16 = (dq, dk, dv)
+ * with the inverse RoPE (table / pos as odc_w_qkv_rope_bwd) applied to the q and k heads;
+ * bit-identical to odc_attn_bwd followed by odc_w_qkv_rope_bwd, one pass instead of four. */
+odc_status odc_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                            const float* lse, const void* table, const int64_t* pos, void* dqkv, void* workspace,
+                            const void* items, int n_items, int64_t T, int H, int KV, int head_dim, float scale,
+                            void* stream);
+
 /* ---------------------------------------------------------------------------
  * Fused elementwise kernels of the SFT worker (csrc/worker_kernels.cu).
  * bf16 tensors row-major and 16-byte aligned; fp32 for rstd / dw / loss.

@@ -85,6 +85,8 @@ SIGNATURES = {
     "odc_attn_fwd": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, C.c_float, vp]),
     "odc_attn_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, C.c_int,
                                C.c_float, vp]),
+    "odc_attn_bwd_qkv": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, C.c_int,
+                                   C.c_float, vp]),
     "odc_w_rmsnorm_fwd": (C.c_int, [vp, vp, vp, vp, i64, C.c_int, C.c_float, vp]),
     "odc_w_rmsnorm_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, vp]),
     "odc_w_qkv_rope_fwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, vp]),

@@ -919,15 +919,80 @@ extern "C" odc_status odc_attn_fwd(const void* q, const void* k, const void* v, 
     });
 }
 
-extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
-                                   const float* lse, void* dq, void* dk, void* dv, void* workspace,
-                                   const void* items, int n_items, std::int64_t T, int H, int KV, int head_dim,
-                                   float scale, void* stream) {
-    return odc::guard([&] {
-        using namespace odc::attn;
+namespace odc {
+namespace attn {
+
+// fp32 dQ/dK/dV accumulators -> the packed qkv gradient [T][(H+2KV)*128] bf16 with the inverse
+// RoPE applied to the q and k heads: dq_convert (x3) + qkv_rope_bwd in one pass. Each value is
+// rounded to bf16 first, exactly as the two-kernel path stores dq/dk/dv, so the result is
+// bit-identical to it (csrc/worker_kernels.cu qkv_rope_bwd_kernel).
+__global__ void qkv_grad_kernel(const float* __restrict__ dq, const float* __restrict__ dk, const float* __restrict__ dv,
+                                const float2* __restrict__ table, const long long* __restrict__ pos,
+                                unsigned short* __restrict__ dqkv, long long T, int H, int KV) {
+    constexpr int half = HD / 2, groups = half / 8;
+    const int heads = H + 2 * KV;
+    const long long total = T * heads * groups;
+    for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int gi = static_cast<int>(idx % groups);
+        const int h = static_cast<int>((idx / groups) % heads);
+        const long long t = idx / (static_cast<long long>(groups) * heads);
+        const float* src;
+        if (h < H) src = dq + (t * H + h) * HD;
+        else if (h < H + KV) src = dk + (t * KV + (h - H)) * HD;
+        else src = dv + (t * KV + (h - H - KV)) * HD;
+        float a[8], b[8];
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src + gi * 8) + q4);
+            const float4 y = __ldg(reinterpret_cast<const float4*>(src + gi * 8 + half) + q4);
+            const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // the bf16 the unfused path stores
+                a[4 * q4 + e] = __bfloat162float(__float2bfloat16_rn(xs[e]));
+                b[4 * q4 + e] = __bfloat162float(__float2bfloat16_rn(ys[e]));
+            }
+        }
+        if (h < H + KV) {
+            const float4* cs4 = reinterpret_cast<const float4*>(table + pos[t] * half + gi * 8);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 u = __ldg(cs4 + q4);
+                const float c0 = u.x, s0 = u.y, c1 = u.z, s1 = u.w;
+                const float y1 = a[2 * q4], y2 = b[2 * q4], z1 = a[2 * q4 + 1], z2 = b[2 * q4 + 1];
+                a[2 * q4] = y1 * c0 + y2 * s0;
+                b[2 * q4] = y2 * c0 - y1 * s0;
+                a[2 * q4 + 1] = z1 * c1 + z2 * s1;
+                b[2 * q4 + 1] = z2 * c1 - z1 * s1;
+            }
+        }
+        const long long dst = t * heads * HD + static_cast<long long>(h) * HD + gi * 8;
+        uint4 pa, pb;
+        pa.x = pack_bf16(a[0], a[1]);
+        pa.y = pack_bf16(a[2], a[3]);
+        pa.z = pack_bf16(a[4], a[5]);
+        pa.w = pack_bf16(a[6], a[7]);
+        pb.x = pack_bf16(b[0], b[1]);
+        pb.y = pack_bf16(b[2], b[3]);
+        pb.z = pack_bf16(b[4], b[5]);
+        pb.w = pack_bf16(b[6], b[7]);
+        *reinterpret_cast<uint4*>(dqkv + dst) = pa;
+        *reinterpret_cast<uint4*>(dqkv + dst + half) = pb;
+    }
+}
+
+}  // namespace attn
+}  // namespace odc
+
+namespace {
+// the backward up to the fp32 accumulators; returns (dq_acc, dk_acc, dv_acc) in the workspace
+void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
+                         void* workspace, const void* items, int n_items, std::int64_t T, int H, int KV, int head_dim,
+                         float scale, cudaStream_t st, float** dq_out, float** dk_out, float** dv_out) {
+    using namespace odc::attn;
+    {
         if (head_dim != HD) throw odcsim::ParamError("attn_bwd: head_dim must be 128");
         if (KV < 1 || H % KV) throw odcsim::ParamError("attn_bwd: H must be a multiple of KV");
-        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         static thread_local int configured = -1;
         int dev = 0;
         cudaGetDevice(&dev);
@@ -971,16 +1036,53 @@ extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, 
             odc::count_launch();
             attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
+        *dq_out = dq_acc;
+        *dk_out = dk_acc;
+        *dv_out = dv_acc;
+    }
+}
+}  // namespace
+
+extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                   const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                                   const void* items, int n_items, std::int64_t T, int H, int KV, int head_dim,
+                                   float scale, void* stream) {
+    return odc::guard([&] {
+        using namespace odc::attn;
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        float *dq_acc, *dk_acc, *dv_acc;
+        attn_bwd_accumulate(q, k, v, o, dout, lse, workspace, items, n_items, T, H, KV, head_dim, scale, st, &dq_acc,
+                            &dk_acc, &dv_acc);
         auto convert = [&](const float* acc, void* out, long long n) {
             odc::count_launch();
             const long long n4 = n / 4;
             dq_convert_kernel<<<static_cast<unsigned>(std::min<long long>((n4 + 255) / 256, 148 * 8)), 256, 0, st>>>(
                 reinterpret_cast<const float4*>(acc), static_cast<uint2*>(out), n4);
         };
-        convert(dq_acc, dq, rows * HD);
+        convert(dq_acc, dq, T * H * HD);
         convert(dk_acc, dk, T * KV * HD);
         convert(dv_acc, dv, T * KV * HD);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw std::runtime_error(std::string("attn_bwd launch: ") + cudaGetErrorString(e));
+    });
+}
+
+extern "C" odc_status odc_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                       const float* lse, const void* table, const int64_t* pos, void* dqkv,
+                                       void* workspace, const void* items, int n_items, std::int64_t T, int H, int KV,
+                                       int head_dim, float scale, void* stream) {
+    return odc::guard([&] {
+        using namespace odc::attn;
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        float *dq_acc, *dk_acc, *dv_acc;
+        attn_bwd_accumulate(q, k, v, o, dout, lse, workspace, items, n_items, T, H, KV, head_dim, scale, st, &dq_acc,
+                            &dk_acc, &dv_acc);
+        const long long n = T * (H + 2 * KV) * (HD / 16);
+        odc::count_launch();
+        qkv_grad_kernel<<<static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(
+            dq_acc, dk_acc, dv_acc, static_cast<const float2*>(table), reinterpret_cast<const long long*>(pos),
+            static_cast<unsigned short*>(dqkv), T, H, KV);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw std::runtime_error(std::string("attn_bwd_qkv launch: ") + cudaGetErrorString(e));
     });
 }

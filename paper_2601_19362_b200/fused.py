@@ -143,3 +143,15 @@ def attn_bwd(q, k, v, o, dout, lse, items, scale):
     check(lib().odc_attn_bwd(_p(q), _p(k), _p(v), _p(o), _p(dout), _p(lse), _p(dq), _p(dk), _p(dv), _p(ws),
                              _p(items), items.shape[0], T, H, KV, hd, float(scale), _s()))
     return dq, dk, dv
+
+
+def attn_bwd_qkv(q, k, v, o, dout, lse, items, scale, table, pos):
+    """The attention backward straight to the packed qkv gradient [T, (H+2KV)*hd]
+    with the inverse RoPE applied (= attn_bwd + qkv_rope_bwd, bit-identical)."""
+    T, H, hd = q.shape
+    KV = k.shape[1]
+    dqkv = torch.empty(T, (H + 2 * KV) * hd, dtype=torch.bfloat16, device=q.device)
+    ws = torch.empty((H * T + 63) // 64 * 64 + T * H * hd + 2 * T * KV * hd, dtype=torch.float32, device=q.device)
+    check(lib().odc_attn_bwd_qkv(_p(q), _p(k), _p(v), _p(o), _p(dout), _p(lse), _p(table), _p(pos), _p(dqkv), _p(ws),
+                                 _p(items), items.shape[0], T, H, KV, hd, float(scale), _s()))
+    return dqkv

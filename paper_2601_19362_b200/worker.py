@@ -473,9 +473,9 @@ class Worker:
             # attention block
             do = G.linear_dgrad(dhm, P["o_w"])
             G.linear_wgrad(dhm, o.view(T, -1), out=Gv["o_w"])
-            dq, dk, dv = F.attn_bwd(q, k, v, o, do.view(T, H, hd), lse, b.attn_bwd_items, scale)
-            dqkv = F.qkv_rope_bwd(dq, dk, dv, tab, b.positions, H, KV, hd)
-            del dq, dk, dv, do
+            # attention backward straight to the packed qkv gradient (inverse RoPE fused)
+            dqkv = F.attn_bwd_qkv(q, k, v, o, do.view(T, H, hd), lse, b.attn_bwd_items, scale, tab, b.positions)
+            del do
             if "qkv_b" in Gv:
                 F.col_sum_(dqkv, Gv["qkv_b"])
             da = G.linear_dgrad(dqkv, P["qkv_w"])

@@ -97,3 +97,28 @@ def test_attn_bwd_matches_reference(lens, H, KV):
         rel = ((got.float() - want).norm() / want.norm().clamp_min(1e-6)).item()
         assert rel < 2e-2 or want.norm() < 1e-4, rel
         torch.testing.assert_close(got.float(), want, rtol=5e-2, atol=5e-2)
+
+
+@pytest.mark.parametrize("lens,H,KV", [([300, 77, 513], 12, 2), ([1000, 2048], 4, 2), ([129, 255], 40, 8)])
+def test_attn_bwd_qkv_matches_unfused(lens, H, KV):
+    """attn_bwd_qkv (accumulators -> packed qkv gradient with the inverse RoPE)
+    performs the roundings of attn_bwd + qkv_rope_bwd (dq/dk/dv to bf16, then
+    the rotation): equal up to the run-to-run order of the fp32 reductions."""
+    from paper_2601_19362_b200 import worker as W
+
+    torch.manual_seed(4)
+    T = sum(lens)
+    q = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
+    k = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    v = torch.randn(T, KV, 128, device=DEV).to(torch.bfloat16)
+    do = torch.randn(T, H, 128, device=DEV).to(torch.bfloat16)
+    scale = 128 ** -0.5
+    pos = torch.cat([torch.arange(n) for n in lens]).to(DEV)
+    tab = F.rope_table(4096, 128, W.ROPE_THETA, DEV)
+    out, lse = F.attn_fwd(q, k, v, F.attn_items(lens, H, DEV), scale)
+    items = F.attn_bwd_items(lens, H, KV, DEV)
+    got = F.attn_bwd_qkv(q, k, v, out, do, lse, items, scale, tab, pos)
+    dq, dk, dv = F.attn_bwd(q, k, v, out, do, lse, items, scale)
+    want = F.qkv_rope_bwd(dq, dk, dv, tab, pos, H, KV, 128)
+    # the fp32 accumulators differ run to run (TMA reduce-add order), so compare to bf16 rounding
+    torch.testing.assert_close(got.float(), want.float(), rtol=1e-2, atol=1e-2)
