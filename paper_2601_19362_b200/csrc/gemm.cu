@@ -109,6 +109,16 @@ struct Args {
     // from glu_gu [M][2*ffn] (bit-identical to swiglu_bwd_kernel on the stored dm)
     const void* glu_gu;
     void* glu_dgu;
+    // fused bias + RoPE + q/k/v split (qkv projection, 2-CTA kernel only): output tile n holds heads
+    // 2n and 2n+1 (128 columns each); the epilogue writes them to rope_q [M][H][128], rope_k / rope_v
+    // [M][KV][128], bias and RoPE applied exactly as qkv_rope_fwd_kernel does on the stored bf16 qkv
+    void* rope_q;
+    void* rope_k;
+    void* rope_v;
+    const void* rope_bias;    // [(H+2KV)*128] bf16 or null
+    const void* rope_table;   // float2 {cos, sin} [max_pos][64]
+    const long long* rope_pos;  // [M]
+    int rope_h, rope_kv;
 };
 
 // swiglu_bwd_kernel's arithmetic on 8 packed bf16 (csrc/worker_kernels.cu swiglu_bwd8)
@@ -490,6 +500,11 @@ __device__ __forceinline__ void reg_fence32(unsigned* r) {
                  : "memory");
 }
 
+// epilogue variants of the 2-CTA kernel, one instantiation each (a fused epilogue's registers
+// never burden the plain GEMM)
+enum Epi : int { kEpiPlain = 0, kEpiGluFwd = 1, kEpiGluBwd = 2, kEpiRope = 3 };
+
+template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Args g) {
     constexpr int BN2 = 256;
@@ -548,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int sp = w % g.splits;
                 const int kb = k_tiles * sp / g.splits, ke = k_tiles * (sp + 1) / g.splits;
                 const int ma = m0 + static_cast<int>(rank) * 128;
-                const int nb = g.glu_m ? (rank ? g.ffn : 0) + n0 / 2 : n0 + static_cast<int>(rank) * 128;
+                const int nb = EPI == kEpiGluFwd ? (rank ? g.ffn : 0) + n0 / 2 : n0 + static_cast<int>(rank) * 128;
                 for (int kt = kb; kt < ke; ++kt, ++it) {
                     const int s = it % kStages2;
                     if (it >= kStages2) mbar_wait(&empty_bar[s], ((it / kStages2) - 1) & 1);
@@ -634,7 +649,92 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             : (g.accumulate ? orow : nullptr);
             const bool fast = !g.d_f32 && n0 + BN2 <= g.N && (reinterpret_cast<uintptr_t>(orow) & 15) == 0 &&
                               (arow == nullptr || (reinterpret_cast<uintptr_t>(arow) & 15) == 0);
-            if (g.glu_dgu) {  // fused SwiGLU backward (host guarantees the fast-path conditions)
+            if constexpr (EPI == kEpiRope) {  // fused bias + RoPE + split (host guarantees the fast-path conditions)
+                const long long p = row_ok ? __ldg(g.rope_pos + row) : 0;
+                const float4* tab = static_cast<const float4*>(g.rope_table) + p * 32;  // 64 (cos, sin) pairs
+                mbar_wait(&tmem_full[acc], use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned tbase = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2);
+#pragma unroll 1
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int h = n0 / 128 + hh;
+                    const bool rot = h < g.rope_h + g.rope_kv;
+                    __nv_bfloat16* dst;
+                    if (h < g.rope_h) dst = static_cast<__nv_bfloat16*>(g.rope_q) + (row * g.rope_h + h) * 128;
+                    else if (rot) dst = static_cast<__nv_bfloat16*>(g.rope_k) + (row * g.rope_kv + h - g.rope_h) * 128;
+                    else dst = static_cast<__nv_bfloat16*>(g.rope_v) + (row * g.rope_kv + h - g.rope_h - g.rope_kv) * 128;
+                    const __nv_bfloat16* bias =
+                        g.rope_bias ? static_cast<const __nv_bfloat16*>(g.rope_bias) + static_cast<long long>(h) * 128 : nullptr;
+#pragma unroll 1
+                    for (int c = 0; c < 2; ++c) {  // columns [32c, 32c+32) pair with [64+32c, 64+32c+32)
+                        unsigned ra[32], rb[32];
+                        tmem_ld32(tbase + hh * 128 + c * 32, ra);
+                        tmem_ld32(tbase + hh * 128 + 64 + c * 32, rb);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        reg_fence32(ra);
+                        reg_fence32(rb);
+                        if (hh == 1 && c == 1) {  // accumulator in registers: release the buffer to the leader's MMA
+                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0)
+                                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                                 leader_empty0 + 8u * acc)
+                                             : "memory");
+                        }
+                        if (!row_ok) continue;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {  // 8 pairs per step
+                            float a[8], b[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {  // the bf16 the unfused GEMM stores
+                                a[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ra[8 * q + e])));
+                                b[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(rb[8 * q + e])));
+                            }
+                            if (bias) {
+                                const uint4 ba = __ldg(reinterpret_cast<const uint4*>(bias + c * 32 + 8 * q));
+                                const uint4 bb = __ldg(reinterpret_cast<const uint4*>(bias + 64 + c * 32 + 8 * q));
+                                const unsigned* wa = reinterpret_cast<const unsigned*>(&ba);
+                                const unsigned* wb = reinterpret_cast<const unsigned*>(&bb);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    a[2 * e] += __uint_as_float(wa[e] << 16);
+                                    a[2 * e + 1] += __uint_as_float(wa[e] & 0xffff0000u);
+                                    b[2 * e] += __uint_as_float(wb[e] << 16);
+                                    b[2 * e + 1] += __uint_as_float(wb[e] & 0xffff0000u);
+                                }
+                            }
+                            if (rot) {
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; ++q4) {
+                                    const float4 u = __ldg(tab + (c * 32 + 8 * q) / 2 + q4);
+                                    const float cc[2] = {u.x, u.z}, sn[2] = {u.y, u.w};
+#pragma unroll
+                                    for (int e = 0; e < 2; ++e) {
+                                        const int j = 2 * q4 + e;
+                                        const float x1 = a[j], x2 = b[j];
+                                        a[j] = x1 * cc[e] - x2 * sn[e];
+                                        b[j] = x2 * cc[e] + x1 * sn[e];
+                                    }
+                                }
+                            }
+                            uint4 pa, pb;
+                            unsigned* wpa = reinterpret_cast<unsigned*>(&pa);
+                            unsigned* wpb = reinterpret_cast<unsigned*>(&pb);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                __nv_bfloat162 x = __floats2bfloat162_rn(a[2 * e], a[2 * e + 1]);
+                                __nv_bfloat162 y = __floats2bfloat162_rn(b[2 * e], b[2 * e + 1]);
+                                wpa[e] = *reinterpret_cast<unsigned*>(&x);
+                                wpb[e] = *reinterpret_cast<unsigned*>(&y);
+                            }
+                            *reinterpret_cast<uint4*>(dst + c * 32 + 8 * q) = pa;
+                            *reinterpret_cast<uint4*>(dst + 64 + c * 32 + 8 * q) = pb;
+                        }
+                    }
+                }
+                continue;
+            }
+            if constexpr (EPI == kEpiGluBwd) {  // fused SwiGLU backward (host guarantees the fast-path conditions)
                 const long long ld2 = 2LL * g.ffn;
                 const __nv_bfloat16* grow = static_cast<const __nv_bfloat16*>(g.glu_gu) + row * ld2 + n0;
                 const __nv_bfloat16* urow = grow + g.ffn;
@@ -687,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 continue;
             }
-            if (g.glu_m) {  // fused SwiGLU (host guarantees the fast-path conditions)
+            if constexpr (EPI == kEpiGluFwd) {  // fused SwiGLU (host guarantees the fast-path conditions)
                 mbar_wait(&tmem_full[acc], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const unsigned tbase = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2);
@@ -889,8 +989,10 @@ cudaError_t launch2(const void* A, const void* B, Args g, long long lda, long lo
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
-        cudaError_t e = cudaFuncSetAttribute(gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
-        if (e != cudaSuccess) return e;
+        for (auto fn : {gemm2_kernel<kEpiPlain>, gemm2_kernel<kEpiGluFwd>, gemm2_kernel<kEpiGluBwd>, gemm2_kernel<kEpiRope>}) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+            if (e != cudaSuccess) return e;
+        }
         configured = dev;
     }
     // per CTA: A half = 128 rows (box 64 x 128 K-major / 2 boxes 64 x 64 MN-major), B half = 128 rows likewise
@@ -921,7 +1023,10 @@ cudaError_t launch2(const void* A, const void* B, Args g, long long lda, long lo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, gemm2_kernel, ma, mb, g);
+    if (g.rope_q) return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiRope>, ma, mb, g);
+    if (g.glu_dgu) return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiGluBwd>, ma, mb, g);
+    if (g.glu_m) return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiGluFwd>, ma, mb, g);
+    return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiPlain>, ma, mb, g);
 }
 
 template <int BN>
@@ -961,6 +1066,48 @@ extern "C" odc_status odc_gemm_set_raster(int group, int l2_budget_mb) {
         if (group < 0 || l2_budget_mb < 0) throw odcsim::ParamError("raster: group and budget must be >= 0");
         odc::gemm::raster_forced().store(group);
         if (l2_budget_mb > 0) odc::gemm::raster_budget().store(static_cast<long long>(l2_budget_mb) << 20);
+    });
+}
+
+extern "C" odc_status odc_gemm_qkv_rope(const void* X, const void* W, const void* bias, const void* table,
+                                        const int64_t* pos, void* q, void* k, void* v, std::int64_t T, std::int64_t d,
+                                        int H, int KV, void* stream) {
+    return odc::guard([&] {
+        using odcsim::ParamError;
+        if (T < 1 || d < 1 || H < 1 || KV < 1) throw ParamError("qkv: dims must be >= 1");
+        if (d % 8) throw ParamError("qkv: d must be a multiple of 8");
+        const void* ops[] = {X, W, q, k, v};
+        for (const void* p : ops)
+            if (reinterpret_cast<uintptr_t>(p) % 16) throw ParamError("qkv: operands must be 16-byte aligned");
+        const std::int64_t N = static_cast<std::int64_t>(H + 2 * KV) * 128;
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (T < 256 || (H + 2 * KV) % 2 || std::getenv("ODC_GEMM_1CTA")) {  // the unfused sm_100a pair
+            void* qkv = nullptr;
+            if (cudaMallocAsync(&qkv, static_cast<size_t>(T * N * 2), st) != cudaSuccess)
+                throw std::runtime_error("qkv: scratch allocation failed");
+            odc_status e = odc_gemm_bf16(X, W, qkv, nullptr, T, N, d, d, d, N, 0, 0, ODC_BF16, 0, stream);
+            if (e == ODC_OK) e = odc_w_qkv_rope_fwd(qkv, bias, table, pos, q, k, v, T, H, KV, 128, stream);
+            cudaFreeAsync(qkv, st);
+            if (e != ODC_OK) throw std::runtime_error(odc_last_error());
+            return;
+        }
+        odc::gemm::Args g{};
+        g.D = q;  // unused by the fused epilogue (kept non-null)
+        g.M = T;
+        g.N = N;
+        g.K = d;
+        g.ldd = N;
+        g.splits = 1;
+        g.rope_q = q;
+        g.rope_k = k;
+        g.rope_v = v;
+        g.rope_bias = bias;
+        g.rope_table = table;
+        g.rope_pos = reinterpret_cast<const long long*>(pos);
+        g.rope_h = H;
+        g.rope_kv = KV;
+        const cudaError_t e = odc::gemm::launch2(X, W, g, d, d, st);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("qkv launch: ") + cudaGetErrorString(e));
     });
 }
 

@@ -361,9 +361,8 @@ class Worker:
         hd, H, KV = s.head_dim, s.heads, s.kv_heads
         T = b.tokens
         a, r1 = F.rmsnorm_fwd(x, P["ln1"])
-        qkv = G.linear_fwd(a, P["qkv_w"])
-        q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), self.rope, b.positions, H, KV, hd)
-        del qkv
+        # qkv projection with bias + RoPE + the q/k/v split fused into the GEMM epilogue
+        q, k, v = G.qkv_rope(a, P["qkv_w"], P.get("qkv_b"), self.rope, b.positions, H, KV)
         if o_lse is not None:
             o, lse = o_lse
         else:

@@ -93,3 +93,22 @@ def test_down_dgrad_swiglu_bwd_fused_matches_unfused(T, d, ffn):
     dmf = dm.float()
     want = torch.cat([dmf * u * sg * (1 + g * (1 - sg)), dmf * g * sg], 1)
     torch.testing.assert_close(dgu.float(), want, rtol=3e-2, atol=3e-2)
+
+
+@pytest.mark.parametrize("T,d,H,KV,bias", [(100, 256, 2, 1, True), (1000, 1536, 12, 2, True), (4097, 512, 4, 1, False),
+                                           (32768, 1536, 12, 2, True), (777, 512, 3, 2, True)])
+def test_qkv_rope_fused_matches_unfused(T, d, H, KV, bias):
+    """bias + RoPE + q/k/v split fused into the qkv GEMM epilogue: bit-identical
+    to the plain GEMM + qkv_rope_fwd kernel (T < 256 or an odd head count run
+    that pair)."""
+    from paper_2601_19362_b200 import fused as F
+    from paper_2601_19362_b200 import worker as W
+
+    N = (H + 2 * KV) * 128
+    x, w = _r(T, d), (torch.randn(N, d, device=DEV) * 0.05).to(torch.bfloat16)
+    b = (torch.randn(N, device=DEV) * 0.1).to(torch.bfloat16) if bias else None
+    pos = (torch.arange(T, device=DEV) * 7) % 3000
+    tab = F.rope_table(4096, 128, W.ROPE_THETA, DEV)
+    q, k, v = G.qkv_rope(x, w, b, tab, pos, H, KV)
+    rq, rk, rv = F.qkv_rope_fwd(G.linear_fwd(x, w), b, tab, pos, H, KV, 128)
+    assert torch.equal(q, rq) and torch.equal(k, rk) and torch.equal(v, rv)
