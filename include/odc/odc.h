@@ -247,19 +247,6 @@ odc_status odc_gemm_set_raster(int group, int l2_budget_mb);
 odc_status odc_gemm_gate_up_swiglu(const void* X, const void* W, void* gu, void* m, int64_t T, int64_t ffn, int64_t d,
                                    void* stream);
 
-/* qkv projection with bias + RoPE + the q/k/v split fused into the epilogue (2-CTA tcgen05 GEMM):
- * q [T][H][128], k / v [T][KV][128] = split(X · W^T + bias) with RoPE on q and k (table / pos as
- * odc_w_qkv_rope_fwd); bit-identical to odc_gemm_bf16 + odc_w_qkv_rope_fwd. head_dim 128. */
-odc_status odc_gemm_qkv_rope(const void* X, const void* W, const void* bias, const void* table, const int64_t* pos,
-                             void* q, void* k, void* v, int64_t T, int64_t d, int H, int KV, void* stream);
-
-/* down-proj dgrad with the SwiGLU backward fused into the epilogue (2-CTA tcgen05 GEMM):
- * dm = dY [T][d] · Wd with Wd [d][ffn] (the down weight as stored) stays in TMEM; the epilogue
- * writes dgu [T][2*ffn] = swiglu_bwd(bf16(dm), gu) (bit-identical to odc_w_swiglu_bwd on the
- * stored dm). gu [T][2*ffn] = the forward's gate|up. ffn % 256 == 0 for the fused path. */
-odc_status odc_gemm_down_dgrad_swiglu_bwd(const void* dY, const void* Wd, const void* gu, void* dgu, int64_t T,
-                                          int64_t ffn, int64_t d, void* stream);
-
 /* Causal varlen flash-attention forward on tcgen05 (head_dim 128, GQA).
  * q [T][H][128], k/v [T][KV][128] bf16; out [T][H][128]; lse [H][T] fp32 (natural log).
  * items: n_items x {seq_start, seq_len, q_tile, head} (int32 x4), one CTA each;

@@ -78,8 +78,6 @@ SIGNATURES = {
     "odc_copy_segments": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), i64p, C.c_int, vp]),
     "odc_l2_flush": (C.c_int, [vp, i64, vp]),
     "odc_gemm_set_raster": (C.c_int, [C.c_int, C.c_int]),
-    "odc_gemm_qkv_rope": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, C.c_int, C.c_int, vp]),
-    "odc_gemm_down_dgrad_swiglu_bwd": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, vp]),
     "odc_gemm_gate_up_swiglu": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, vp]),
     "odc_gemm_bf16": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int,
                                 vp]),

@@ -103,47 +103,7 @@ struct Args {
     // glu_m = silu(g) * u [M][ffn] (from the bf16-rounded g, u: bit-identical to swiglu_fwd)
     void* glu_m;
     int ffn;
-    // fused SwiGLU backward (down-proj dgrad, 2-CTA kernel only): the accumulator is dm = dY · W_down
-    // [M][ffn]; instead of storing it the epilogue rounds it to bf16 and writes
-    // glu_dgu [M][2*ffn] = (dm * u * s * (1 + g * (1 - s)), dm * g * s), s = sigmoid(g), with g, u read
-    // from glu_gu [M][2*ffn] (bit-identical to swiglu_bwd_kernel on the stored dm)
-    const void* glu_gu;
-    void* glu_dgu;
-    // fused bias + RoPE + q/k/v split (qkv projection, 2-CTA kernel only): output tile n holds heads
-    // 2n and 2n+1 (128 columns each); the epilogue writes them to rope_q [M][H][128], rope_k / rope_v
-    // [M][KV][128], bias and RoPE applied exactly as qkv_rope_fwd_kernel does on the stored bf16 qkv
-    void* rope_q;
-    void* rope_k;
-    void* rope_v;
-    const void* rope_bias;    // [(H+2KV)*128] bf16 or null
-    const void* rope_table;   // float2 {cos, sin} [max_pos][64]
-    const long long* rope_pos;  // [M]
-    int rope_h, rope_kv;
 };
-
-// swiglu_bwd_kernel's arithmetic on 8 packed bf16 (csrc/worker_kernels.cu swiglu_bwd8)
-__device__ __forceinline__ void glu_bwd8(const unsigned* dm, const uint4& gv, const uint4& uv, uint4& dgo, uint4& duo) {
-    const unsigned* gw = reinterpret_cast<const unsigned*>(&gv);
-    const unsigned* uw = reinterpret_cast<const unsigned*>(&uv);
-    unsigned* dg = reinterpret_cast<unsigned*>(&dgo);
-    unsigned* du = reinterpret_cast<unsigned*>(&duo);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        float d[2], g[2], u[2], rg[2], ru[2];
-        d[0] = __uint_as_float(dm[e] << 16), d[1] = __uint_as_float(dm[e] & 0xffff0000u);
-        g[0] = __uint_as_float(gw[e] << 16), g[1] = __uint_as_float(gw[e] & 0xffff0000u);
-        u[0] = __uint_as_float(uw[e] << 16), u[1] = __uint_as_float(uw[e] & 0xffff0000u);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const float sg = __frcp_rn(1.f + __expf(-g[k]));
-            rg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
-            ru[k] = d[k] * g[k] * sg;
-        }
-        __nv_bfloat162 a = __floats2bfloat162_rn(rg[0], rg[1]), b = __floats2bfloat162_rn(ru[0], ru[1]);
-        dg[e] = *reinterpret_cast<unsigned*>(&a);
-        du[e] = *reinterpret_cast<unsigned*>(&b);
-    }
-}
 
 // Tile raster (L2 reuse). Tiles are walked in groups of `group` M-tiles, the
 // N-tiles swept inside a group, so the group's A rows stay in L2 while B
@@ -502,7 +462,7 @@ __device__ __forceinline__ void reg_fence32(unsigned* r) {
 
 // epilogue variants of the 2-CTA kernel, one instantiation each (a fused epilogue's registers
 // never burden the plain GEMM)
-enum Epi : int { kEpiPlain = 0, kEpiGluFwd = 1, kEpiGluBwd = 2, kEpiRope = 3 };
+enum Epi : int { kEpiPlain = 0, kEpiGluFwd = 1 };
 
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -649,144 +609,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             : (g.accumulate ? orow : nullptr);
             const bool fast = !g.d_f32 && n0 + BN2 <= g.N && (reinterpret_cast<uintptr_t>(orow) & 15) == 0 &&
                               (arow == nullptr || (reinterpret_cast<uintptr_t>(arow) & 15) == 0);
-            if constexpr (EPI == kEpiRope) {  // fused bias + RoPE + split (host guarantees the fast-path conditions)
-                const long long p = row_ok ? __ldg(g.rope_pos + row) : 0;
-                const float4* tab = static_cast<const float4*>(g.rope_table) + p * 32;  // 64 (cos, sin) pairs
-                mbar_wait(&tmem_full[acc], use & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const unsigned tbase = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2);
-#pragma unroll 1
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int h = n0 / 128 + hh;
-                    const bool rot = h < g.rope_h + g.rope_kv;
-                    __nv_bfloat16* dst;
-                    if (h < g.rope_h) dst = static_cast<__nv_bfloat16*>(g.rope_q) + (row * g.rope_h + h) * 128;
-                    else if (rot) dst = static_cast<__nv_bfloat16*>(g.rope_k) + (row * g.rope_kv + h - g.rope_h) * 128;
-                    else dst = static_cast<__nv_bfloat16*>(g.rope_v) + (row * g.rope_kv + h - g.rope_h - g.rope_kv) * 128;
-                    const __nv_bfloat16* bias =
-                        g.rope_bias ? static_cast<const __nv_bfloat16*>(g.rope_bias) + static_cast<long long>(h) * 128 : nullptr;
-#pragma unroll 1
-                    for (int c = 0; c < 2; ++c) {  // columns [32c, 32c+32) pair with [64+32c, 64+32c+32)
-                        unsigned ra[32], rb[32];
-                        tmem_ld32(tbase + hh * 128 + c * 32, ra);
-                        tmem_ld32(tbase + hh * 128 + 64 + c * 32, rb);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        reg_fence32(ra);
-                        reg_fence32(rb);
-                        if (hh == 1 && c == 1) {  // accumulator in registers: release the buffer to the leader's MMA
-                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                            __syncwarp();
-                            if (lane == 0)
-                                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                                                 leader_empty0 + 8u * acc)
-                                             : "memory");
-                        }
-                        if (!row_ok) continue;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {  // 8 pairs per step
-                            float a[8], b[8];
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {  // the bf16 the unfused GEMM stores
-                                a[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ra[8 * q + e])));
-                                b[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(rb[8 * q + e])));
-                            }
-                            if (bias) {
-                                const uint4 ba = __ldg(reinterpret_cast<const uint4*>(bias + c * 32 + 8 * q));
-                                const uint4 bb = __ldg(reinterpret_cast<const uint4*>(bias + 64 + c * 32 + 8 * q));
-                                const unsigned* wa = reinterpret_cast<const unsigned*>(&ba);
-                                const unsigned* wb = reinterpret_cast<const unsigned*>(&bb);
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    a[2 * e] += __uint_as_float(wa[e] << 16);
-                                    a[2 * e + 1] += __uint_as_float(wa[e] & 0xffff0000u);
-                                    b[2 * e] += __uint_as_float(wb[e] << 16);
-                                    b[2 * e + 1] += __uint_as_float(wb[e] & 0xffff0000u);
-                                }
-                            }
-                            if (rot) {
-#pragma unroll
-                                for (int q4 = 0; q4 < 4; ++q4) {
-                                    const float4 u = __ldg(tab + (c * 32 + 8 * q) / 2 + q4);
-                                    const float cc[2] = {u.x, u.z}, sn[2] = {u.y, u.w};
-#pragma unroll
-                                    for (int e = 0; e < 2; ++e) {
-                                        const int j = 2 * q4 + e;
-                                        const float x1 = a[j], x2 = b[j];
-                                        a[j] = x1 * cc[e] - x2 * sn[e];
-                                        b[j] = x2 * cc[e] + x1 * sn[e];
-                                    }
-                                }
-                            }
-                            uint4 pa, pb;
-                            unsigned* wpa = reinterpret_cast<unsigned*>(&pa);
-                            unsigned* wpb = reinterpret_cast<unsigned*>(&pb);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                __nv_bfloat162 x = __floats2bfloat162_rn(a[2 * e], a[2 * e + 1]);
-                                __nv_bfloat162 y = __floats2bfloat162_rn(b[2 * e], b[2 * e + 1]);
-                                wpa[e] = *reinterpret_cast<unsigned*>(&x);
-                                wpb[e] = *reinterpret_cast<unsigned*>(&y);
-                            }
-                            *reinterpret_cast<uint4*>(dst + c * 32 + 8 * q) = pa;
-                            *reinterpret_cast<uint4*>(dst + 64 + c * 32 + 8 * q) = pb;
-                        }
-                    }
-                }
-                continue;
-            }
-            if constexpr (EPI == kEpiGluBwd) {  // fused SwiGLU backward (host guarantees the fast-path conditions)
-                const long long ld2 = 2LL * g.ffn;
-                const __nv_bfloat16* grow = static_cast<const __nv_bfloat16*>(g.glu_gu) + row * ld2 + n0;
-                const __nv_bfloat16* urow = grow + g.ffn;
-                __nv_bfloat16* dgrow = static_cast<__nv_bfloat16*>(g.glu_dgu) + row * ld2 + n0;
-                __nv_bfloat16* durow = dgrow + g.ffn;
-                uint4 gu_cur[8], gu_nxt[8];  // g (4 x 16 B) and u (4 x 16 B) of one 32-column chunk
-                auto load_gu = [&](int c, uint4* dst) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        dst[q] = __ldg(reinterpret_cast<const uint4*>(grow + c * 32) + q);
-                        dst[4 + q] = __ldg(reinterpret_cast<const uint4*>(urow + c * 32) + q);
-                    }
-                };
-                if (row_ok) load_gu(0, gu_cur);  // in flight while the MMAs run
-                mbar_wait(&tmem_full[acc], use & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const unsigned tbase = tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * BN2);
-#pragma unroll
-                for (int c = 0; c < BN2 / 32; ++c) {
-                    unsigned r[32];
-                    tmem_ld32(tbase + c * 32, r);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    reg_fence32(r);
-                    if (c + 1 == BN2 / 32) {  // accumulator in registers: release the buffer to the leader's MMA
-                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                        __syncwarp();
-                        if (lane == 0)
-                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                                             leader_empty0 + 8u * acc)
-                                         : "memory");
-                    }
-                    if (!row_ok) continue;
-                    uint4* cur = (c & 1) ? gu_nxt : gu_cur;
-                    uint4* nxt = (c & 1) ? gu_cur : gu_nxt;
-                    if (c + 1 < BN2 / 32) load_gu(c + 1, nxt);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        unsigned dm[4];  // dm rounded to bf16, as the unfused dgrad stores it
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * q + 2 * e]),
-                                                                     __uint_as_float(r[8 * q + 2 * e + 1]));
-                            dm[e] = *reinterpret_cast<unsigned*>(&h);
-                        }
-                        uint4 dgv, duv;
-                        glu_bwd8(dm, cur[q], cur[4 + q], dgv, duv);
-                        *reinterpret_cast<uint4*>(dgrow + c * 32 + 8 * q) = dgv;
-                        *reinterpret_cast<uint4*>(durow + c * 32 + 8 * q) = duv;
-                    }
-                }
-                continue;
-            }
             if constexpr (EPI == kEpiGluFwd) {  // fused SwiGLU (host guarantees the fast-path conditions)
                 mbar_wait(&tmem_full[acc], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -989,7 +811,7 @@ cudaError_t launch2(const void* A, const void* B, Args g, long long lda, long lo
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
-        for (auto fn : {gemm2_kernel<kEpiPlain>, gemm2_kernel<kEpiGluFwd>, gemm2_kernel<kEpiGluBwd>, gemm2_kernel<kEpiRope>}) {
+        for (auto fn : {gemm2_kernel<kEpiPlain>, gemm2_kernel<kEpiGluFwd>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
             if (e != cudaSuccess) return e;
         }
@@ -1023,8 +845,6 @@ cudaError_t launch2(const void* A, const void* B, Args g, long long lda, long lo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     count_launch();
-    if (g.rope_q) return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiRope>, ma, mb, g);
-    if (g.glu_dgu) return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiGluBwd>, ma, mb, g);
     if (g.glu_m) return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiGluFwd>, ma, mb, g);
     return cudaLaunchKernelEx(&cfg, gemm2_kernel<kEpiPlain>, ma, mb, g);
 }
@@ -1066,84 +886,6 @@ extern "C" odc_status odc_gemm_set_raster(int group, int l2_budget_mb) {
         if (group < 0 || l2_budget_mb < 0) throw odcsim::ParamError("raster: group and budget must be >= 0");
         odc::gemm::raster_forced().store(group);
         if (l2_budget_mb > 0) odc::gemm::raster_budget().store(static_cast<long long>(l2_budget_mb) << 20);
-    });
-}
-
-extern "C" odc_status odc_gemm_qkv_rope(const void* X, const void* W, const void* bias, const void* table,
-                                        const int64_t* pos, void* q, void* k, void* v, std::int64_t T, std::int64_t d,
-                                        int H, int KV, void* stream) {
-    return odc::guard([&] {
-        using odcsim::ParamError;
-        if (T < 1 || d < 1 || H < 1 || KV < 1) throw ParamError("qkv: dims must be >= 1");
-        if (d % 8) throw ParamError("qkv: d must be a multiple of 8");
-        const void* ops[] = {X, W, q, k, v};
-        for (const void* p : ops)
-            if (reinterpret_cast<uintptr_t>(p) % 16) throw ParamError("qkv: operands must be 16-byte aligned");
-        const std::int64_t N = static_cast<std::int64_t>(H + 2 * KV) * 128;
-        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        if (T < 256 || (H + 2 * KV) % 2 || std::getenv("ODC_GEMM_1CTA")) {  // the unfused sm_100a pair
-            void* qkv = nullptr;
-            if (cudaMallocAsync(&qkv, static_cast<size_t>(T * N * 2), st) != cudaSuccess)
-                throw std::runtime_error("qkv: scratch allocation failed");
-            odc_status e = odc_gemm_bf16(X, W, qkv, nullptr, T, N, d, d, d, N, 0, 0, ODC_BF16, 0, stream);
-            if (e == ODC_OK) e = odc_w_qkv_rope_fwd(qkv, bias, table, pos, q, k, v, T, H, KV, 128, stream);
-            cudaFreeAsync(qkv, st);
-            if (e != ODC_OK) throw std::runtime_error(odc_last_error());
-            return;
-        }
-        odc::gemm::Args g{};
-        g.D = q;  // unused by the fused epilogue (kept non-null)
-        g.M = T;
-        g.N = N;
-        g.K = d;
-        g.ldd = N;
-        g.splits = 1;
-        g.rope_q = q;
-        g.rope_k = k;
-        g.rope_v = v;
-        g.rope_bias = bias;
-        g.rope_table = table;
-        g.rope_pos = reinterpret_cast<const long long*>(pos);
-        g.rope_h = H;
-        g.rope_kv = KV;
-        const cudaError_t e = odc::gemm::launch2(X, W, g, d, d, st);
-        if (e != cudaSuccess) throw std::runtime_error(std::string("qkv launch: ") + cudaGetErrorString(e));
-    });
-}
-
-extern "C" odc_status odc_gemm_down_dgrad_swiglu_bwd(const void* dY, const void* Wd, const void* gu, void* dgu,
-                                                     std::int64_t T, std::int64_t ffn, std::int64_t d, void* stream) {
-    return odc::guard([&] {
-        using odcsim::ParamError;
-        if (T < 1 || ffn < 1 || d < 1) throw ParamError("down dgrad: dims must be >= 1");
-        if (ffn % 8 || d % 8) throw ParamError("down dgrad: ffn and d must be multiples of 8");
-        if (reinterpret_cast<uintptr_t>(dY) % 16 || reinterpret_cast<uintptr_t>(Wd) % 16 ||
-            reinterpret_cast<uintptr_t>(gu) % 16 || reinterpret_cast<uintptr_t>(dgu) % 16)
-            throw ParamError("down dgrad: operands must be 16-byte aligned");
-        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        if (T < 256 || ffn % 256 || std::getenv("ODC_GEMM_1CTA")) {  // the unfused sm_100a pair
-            void* dm = nullptr;
-            if (cudaMallocAsync(&dm, static_cast<size_t>(T * ffn * 2), st) != cudaSuccess)
-                throw std::runtime_error("down dgrad: scratch allocation failed");
-            odc_status e = odc_gemm_bf16(dY, Wd, dm, nullptr, T, ffn, d, d, ffn, ffn, 0, 1, ODC_BF16, 0, stream);
-            if (e == ODC_OK) e = odc_w_swiglu_bwd(dm, gu, dgu, T, static_cast<int>(ffn), stream);
-            cudaFreeAsync(dm, st);
-            if (e != ODC_OK) throw std::runtime_error(odc_last_error());
-            return;
-        }
-        odc::gemm::Args g{};
-        g.D = dgu;  // unused by the fused epilogue (kept non-null)
-        g.M = T;
-        g.N = ffn;
-        g.K = d;
-        g.ldd = 2 * ffn;
-        g.b_mn = 1;
-        g.splits = 1;
-        g.ffn = static_cast<int>(ffn);
-        g.glu_gu = gu;
-        g.glu_dgu = dgu;
-        const cudaError_t e = odc::gemm::launch2(dY, Wd, g, d, ffn, st);
-        if (e != cudaSuccess) throw std::runtime_error(std::string("down dgrad launch: ") + cudaGetErrorString(e));
     });
 }
 

@@ -97,45 +97,3 @@ def gate_up_swiglu(x, w, ffn):
         rec.rows.append((2.0 * T * 2 * ffn * d, e0, e1, (T, 2 * ffn, d, 0, 0, False, False, "glu")))
     return gu, m
 
-
-def down_dgrad_swiglu_bwd(dh, w_down, gu, ffn):
-    """dgu = swiglu_bwd(dh · w_down, gu) with the SwiGLU backward fused into the
-    dgrad GEMM's epilogue (csrc/gemm.cu glu_dgu mode): dm never reaches HBM.
-    dh [T, d], w_down [d, ffn], gu [T, 2*ffn] -> dgu [T, 2*ffn]."""
-    T, d = dh.shape
-    assert w_down.shape == (d, ffn) and gu.shape == (T, 2 * ffn)
-    dgu = torch.empty_like(gu)
-    s = torch.cuda.current_stream()
-    rec = recorder
-    if rec is not None:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-    check(lib().odc_gemm_down_dgrad_swiglu_bwd(_p(dh), _p(w_down), _p(gu), _p(dgu), T, ffn, d,
-                                                C.c_void_p(s.cuda_stream)))
-    if rec is not None:
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record(s)
-        rec.rows.append((2.0 * T * ffn * d, e0, e1, (T, ffn, d, 0, 1, False, False, "glu_bwd")))
-    return dgu
-
-
-def qkv_rope(x, w, bias, table, pos, H, KV):
-    """q, k, v = split(x·wᵀ + bias) with RoPE on q and k, fused into the qkv
-    GEMM's epilogue (csrc/gemm.cu rope mode; head_dim 128)."""
-    T, d = x.shape
-    assert w.shape == ((H + 2 * KV) * 128, d)
-    q = torch.empty(T, H, 128, dtype=torch.bfloat16, device=x.device)
-    k = torch.empty(T, KV, 128, dtype=torch.bfloat16, device=x.device)
-    v = torch.empty(T, KV, 128, dtype=torch.bfloat16, device=x.device)
-    s = torch.cuda.current_stream()
-    rec = recorder
-    if rec is not None:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-    check(lib().odc_gemm_qkv_rope(_p(x), _p(w), None if bias is None else _p(bias), _p(table), _p(pos), _p(q), _p(k),
-                                  _p(v), T, d, H, KV, C.c_void_p(s.cuda_stream)))
-    if rec is not None:
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record(s)
-        rec.rows.append((2.0 * T * (H + 2 * KV) * 128 * d, e0, e1, (T, (H + 2 * KV) * 128, d, 0, 0, False, False, "qkv")))
-    return q, k, v

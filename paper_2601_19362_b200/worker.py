@@ -361,8 +361,9 @@ class Worker:
         hd, H, KV = s.head_dim, s.heads, s.kv_heads
         T = b.tokens
         a, r1 = F.rmsnorm_fwd(x, P["ln1"])
-        # qkv projection with bias + RoPE + the q/k/v split fused into the GEMM epilogue
-        q, k, v = G.qkv_rope(a, P["qkv_w"], P.get("qkv_b"), self.rope, b.positions, H, KV)
+        qkv = G.linear_fwd(a, P["qkv_w"])
+        q, k, v = F.qkv_rope_fwd(qkv, P.get("qkv_b"), self.rope, b.positions, H, KV, hd)
+        del qkv
         if o_lse is not None:
             o, lse = o_lse
         else:
@@ -463,8 +464,10 @@ class Worker:
             tr = self.tracer.span("bwd", l, cur, False) if self.tracer else None
             x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = self._restore(P, saved[l - 1], b)
             # MLP block
-            dgu = G.down_dgrad_swiglu_bwd(dh, P["down_w"], gu, s.ffn)  # SwiGLU bwd in the dgrad epilogue
+            dm = G.linear_dgrad(dh, P["down_w"])
             G.linear_wgrad(dh, m, out=Gv["down_w"])
+            dgu = F.swiglu_bwd(dm, gu, s.ffn)
+            del dm
             dbn = G.linear_dgrad(dgu, P["gu_w"])
             G.linear_wgrad(dgu, bn, out=Gv["gu_w"])
             del dgu

@@ -73,42 +73,3 @@ def test_gate_up_swiglu_fused_matches_unfused(T, d, ffn):
     g, u = gu_ref.float()[:, :ffn], gu_ref.float()[:, ffn:]
     torch.testing.assert_close(m.float(), torch.nn.functional.silu(g) * u, rtol=2e-2, atol=2e-2)
 
-
-@pytest.mark.parametrize("T,d,ffn", [(100, 256, 512), (1000, 1536, 8960), (4097, 512, 1024), (32768, 1536, 8960),
-                                     (600, 256, 640)])
-def test_down_dgrad_swiglu_bwd_fused_matches_unfused(T, d, ffn):
-    """SwiGLU backward fused into the down-proj dgrad epilogue: dgu
-    bit-identical to the plain dgrad (dm stored as bf16) followed by the
-    standalone swiglu_bwd kernel (T < 256 or ffn % 256 != 0 run that pair)."""
-    from paper_2601_19362_b200 import fused as F
-
-    dh = _r(T, d)
-    w_down = (torch.randn(d, ffn, device=DEV) * 0.05).to(torch.bfloat16)
-    gu = _r(T, 2 * ffn)
-    dgu = G.down_dgrad_swiglu_bwd(dh, w_down, gu, ffn)
-    dm = G.linear_dgrad(dh, w_down)
-    assert torch.equal(dgu, F.swiglu_bwd(dm, gu, ffn))
-    g, u = gu.float()[:, :ffn], gu.float()[:, ffn:]
-    sg = torch.sigmoid(g)
-    dmf = dm.float()
-    want = torch.cat([dmf * u * sg * (1 + g * (1 - sg)), dmf * g * sg], 1)
-    torch.testing.assert_close(dgu.float(), want, rtol=3e-2, atol=3e-2)
-
-
-@pytest.mark.parametrize("T,d,H,KV,bias", [(100, 256, 2, 1, True), (1000, 1536, 12, 2, True), (4097, 512, 4, 1, False),
-                                           (32768, 1536, 12, 2, True), (777, 512, 3, 2, True)])
-def test_qkv_rope_fused_matches_unfused(T, d, H, KV, bias):
-    """bias + RoPE + q/k/v split fused into the qkv GEMM epilogue: bit-identical
-    to the plain GEMM + qkv_rope_fwd kernel (T < 256 or an odd head count run
-    that pair)."""
-    from paper_2601_19362_b200 import fused as F
-    from paper_2601_19362_b200 import worker as W
-
-    N = (H + 2 * KV) * 128
-    x, w = _r(T, d), (torch.randn(N, d, device=DEV) * 0.05).to(torch.bfloat16)
-    b = (torch.randn(N, device=DEV) * 0.1).to(torch.bfloat16) if bias else None
-    pos = (torch.arange(T, device=DEV) * 7) % 3000
-    tab = F.rope_table(4096, 128, W.ROPE_THETA, DEV)
-    q, k, v = G.qkv_rope(x, w, b, tab, pos, H, KV)
-    rq, rk, rv = F.qkv_rope_fwd(G.linear_fwd(x, w), b, tab, pos, H, KV, 128)
-    assert torch.equal(q, rq) and torch.equal(k, rk) and torch.equal(v, rv)
