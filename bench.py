@@ -63,7 +63,9 @@ def parse():
     ap.add_argument("--cache-params", action="store_true",
                     help="SURVEY 8(f)1: keep fetched units for the whole minibatch (one fetch per unit per step)")
     ap.add_argument("--model", default="qwen2.5-1.5b")
-    ap.add_argument("--push-mode", default="red", choices=["red", "slot", "fixed"])
+    ap.add_argument("--push-mode", default="slot", choices=["red", "slot", "fixed"],
+                    help="slot (default): deterministic, w*g stored into the owner-side slots; red: remote fp32 reductions; "
+                         "fixed: deterministic int64 fixed point in bounded memory")
     ap.add_argument("--minibs", type=int, default=8)
     ap.add_argument("--fetch-ctas", type=int, default=0)
     ap.add_argument("--push-ctas", type=int, default=0)
