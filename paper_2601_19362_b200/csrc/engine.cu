@@ -49,8 +49,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <unordered_map>
-#include <utility>
 #include <vector>
 
 #include "common.hpp"
@@ -116,11 +114,14 @@ struct odc_ctx {
     std::vector<char> touched;   // SLOT: [unit][owner] this client wrote its slot at the owner this minibatch
     std::int64_t off_marks = -1;  // SLOT: [unit][client] u64 "pushed in minibatch" marks (owner side)
     bool grads_pending = false;  // RED: the grad shards hold a finished minibatch not yet consumed
-    // Per stream: the parameter epoch / drain epoch whose gate kernel was already issued on it
-    // (stream order then covers every later fetch / push on that stream). The waits live in one
-    // tiny gate kernel instead of the data-path kernels, so a waiting rank never holds SMs that
-    // the rank it waits for needs (several ranks per GPU in one process).
-    std::unordered_map<cudaStream_t, std::pair<std::uint64_t, std::uint64_t>> gated;
+    // The waits live in one tiny gate kernel instead of the data-path kernels, so a waiting rank
+    // never holds SMs that the rank it waits for needs (several ranks per GPU in one process).
+    // Per kind (0 parameter epoch, 1 drain epoch): the epoch the last gate kernel waited for and
+    // an event recorded right after it; a later call for the same epoch on any stream just waits
+    // on that event (no kernel, and correct for streams created after the gate).
+    std::uint64_t gate_need[2] = {0, 0};
+    bool gate_issued[2] = {false, false};
+    cudaEvent_t gate_ev[2] = {nullptr, nullptr};
     odc::AdamSeg* d_segs = nullptr;
     std::int64_t* d_seg_start = nullptr;
     std::int64_t adam_units = 0;
@@ -189,16 +190,20 @@ struct odc_ctx {
     // >= adams (param = true: fetch) or drain epoch >= mb_epoch (push), once per
     // stream and epoch.
     void gate(bool param, cudaStream_t s) {
+        const int k = param ? 0 : 1;
         const std::uint64_t need = param ? adams : mb_epoch;
-        auto it = gated.find(s);
-        if (it == gated.end()) it = gated.emplace(s, std::make_pair(~0ull, ~0ull)).first;
-        std::uint64_t& done = param ? it->second.first : it->second.second;
-        if (done != ~0ull && done >= need) return;
+        if (need == 0) return;  // epoch 0 is every flag's initial value
+        if (gate_issued[k] && gate_need[k] >= need) {
+            cuda_ok(cudaStreamWaitEvent(s, gate_ev[k], 0), "wait gate");
+            return;
+        }
         const unsigned long long* g[odc::kMaxSeg];
         for (int r = 0; r < world(); ++r) g[r] = param ? epoch_of(r) : drain_of(r);
-        if (need > 0)  // epoch 0 is every flag's initial value
-            cuda_ok(odc::launch_gated_zero(nullptr, nullptr, 0, g, world(), need, err(), timeout_ns, s), "gate");
-        done = need;
+        cuda_ok(odc::launch_gated_zero(nullptr, nullptr, 0, g, world(), need, err(), timeout_ns, s), "gate");
+        if (!gate_ev[k]) cuda_ok(cudaEventCreateWithFlags(&gate_ev[k], cudaEventDisableTiming), "gate event");
+        cuda_ok(cudaEventRecord(gate_ev[k], s), "record gate");
+        gate_need[k] = need;
+        gate_issued[k] = true;
     }
     // rotation: rank r visits owners r+1, r+2, ..., r so that concurrent
     // fetches/pushes from all ranks spread over all owners' links
@@ -343,6 +348,8 @@ odc_status odc_ctx_destroy(odc_ctx_t c) {
             cudaIpcCloseMemHandle(c->peer[static_cast<std::size_t>(r)]);
     if (c->arena) cudaFree(c->arena);
     if (c->d_segs) cudaFree(c->d_segs);
+    for (cudaEvent_t e : c->gate_ev)
+        if (e) cudaEventDestroy(e);
     if (c->d_seg_start) cudaFree(c->d_seg_start);
     delete c;
     return ODC_OK;
