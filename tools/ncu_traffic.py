@@ -24,7 +24,7 @@ METRICS = {
     "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum": "ops",
     "sm__inst_executed_pipe_tc.sum": "tcinst",
 }
-SCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+SCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
          "KB": 1e3, "MB": 1e6, "GB": 1e9, "%": 1.0, "": 1.0}
 
 KEYS = {"gemm2_kernel": "gemm::gemm2_kernel", "gemm_kernel<256>": "gemm::gemm_kernel<256>",
@@ -42,8 +42,12 @@ def short(name):
 
 
 def main(rep, out, source, launches=None):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
-                         capture_output=True, text=True, check=True).stdout
+    """rep: an .ncu-rep, or the CSV of `ncu -i REP --page raw --csv` exported on the GPU box."""
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO("\n".join(l for l in txt.splitlines() if not l.startswith("==")))))
     head, units = rows[0], rows[1]
     col = {h: i for i, h in enumerate(head)}
