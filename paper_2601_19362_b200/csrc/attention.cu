@@ -26,7 +26,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -523,11 +522,6 @@ __device__ __forceinline__ void stage_f32(char* stage, int r, int c0, const unsi
     }
 }
 
-// Variants (A/B, ODC_ATTN_BWD_VAR): bit 0 — one exp2 pair in two on the FMA pipe (MUFU.EX2 alone
-// needs 1,024 clk per iteration for the 16K probabilities); bit 1 — dQ_n issued before dV_n / dK_n
-// with its own commit, so dQ is read out (and dP_{n+1} may start) while dV and dK run; the dQ
-// staging, which aliases P / dS, then waits for a second commit after dK.
-template <int VAR>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
@@ -546,8 +540,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
     // s_read: S_n, dP_n are in the elementwise warps' registers (S columns free for S_{n+1})
     __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, s_read,
-        ds_full, dq_full, dq_read, pds_free;
-    constexpr bool kPoly = VAR & 1, kDqFirst = (VAR & 2) != 0;
+        ds_full, dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
     const BwdItem it = g.items[blockIdx.x];
@@ -585,7 +578,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
         mbar_init(&dq_read, 8);
-        mbar_init(&pds_free, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -657,15 +649,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
                 mbar_wait(&ds_full, n & 1);  // P, dS in smem
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if constexpr (kDqFirst) {
-#pragma unroll
-                    for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
-                        const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                        mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km,
-                            kk > 0);
-                    }
-                    commit(&dq_full);
-                }
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk)  // K = query rows: MN-major A (P^T) and B (dO)
                     mma(tmem + T_DV, sdesc(pa + kk * 2048, kTile / 2, 1024), sdesc(doa + kk * 2048, kTile / 2, 1024),
@@ -676,17 +659,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma(tmem + T_DK, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024),
                         id_mm, (n > 0 || kk > 0));
                 commit(&q_empty[b]);
-                if constexpr (kDqFirst) {
-                    commit(&pds_free);  // P, dS consumed: the dQ staging may overwrite them
-                } else {
 #pragma unroll
-                    for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
-                        const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                        mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km,
-                            kk > 0);
-                    }
-                    commit(&dq_full);  // also: P, dS consumed
+                for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
+                    const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
                 }
+                commit(&dq_full);  // also: P, dS consumed
             }
         }
       }
@@ -741,7 +719,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
                 for (int x = 0; x < 64; x += 2) {
                     const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
-                    const float2 pp = (kPoly && (x & 2)) ? ex2_fma2(t) : make_float2(ex2(t.x), ex2(t.y));
+                    const float2 pp = make_float2(ex2(t.x), ex2(t.y));
                     const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
                     const float2 d = fmul2(pp, u);
                     sv[x / 2] = pack_bf16(pp.x, pp.y);
@@ -781,7 +759,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&dq_read);
-            if constexpr (kDqFirst) mbar_wait(&pds_free, n & 1);  // dV_n, dK_n done reading P / dS
             stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bar_ew();
@@ -1024,10 +1001,8 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
         int dev = 0;
         cudaGetDevice(&dev);
         if (configured != dev) {
-            for (auto fn : {attn_bwd_kernel<0>, attn_bwd_kernel<1>, attn_bwd_kernel<2>, attn_bwd_kernel<3>}) {
-                cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-                if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
-            }
+            cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+            if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
         // workspace (fp32): D [H][T] | dq_acc [T][H][HD] | dk_acc, dv_acc [T][KV][HD]
@@ -1063,16 +1038,7 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
             a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
-            static const int var = [] {
-                const char* v = std::getenv("ODC_ATTN_BWD_VAR");
-                return v ? std::atoi(v) & 3 : 0;
-            }();
-            switch (var) {
-                case 1: attn_bwd_kernel<1><<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a); break;
-                case 2: attn_bwd_kernel<2><<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a); break;
-                case 3: attn_bwd_kernel<3><<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a); break;
-                default: attn_bwd_kernel<0><<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
-            }
+            attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
         *dq_out = dq_acc;
         *dk_out = dk_acc;

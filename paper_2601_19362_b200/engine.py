@@ -150,19 +150,25 @@ class OdcEngine:
         cfg = _lib.OdcAdamCfg(lr, betas[0], betas[1], eps, weight_decay, self.adam_steps)
         check(lib().odc_adam_step(self.h, C.byref(cfg), _stream(stream)))
 
-    def read_grad_shard(self, layer: int, stream=None) -> torch.Tensor:
+    def _read_shard(self, fn, layer: int, stream=None) -> torch.Tensor:
+        """The copy runs on `stream`; the current stream is made to wait for it, so
+        the returned tensor is safe to use (e.g. .cpu()) on the current stream."""
         _, n = self.shard_range(layer)
         out = torch.empty(max(n, 1), dtype=torch.float32, device=f"cuda:{self.device}")[:n]
         if n:
-            check(lib().odc_read_grad_shard(self.h, layer, _ptr(out), _stream(stream)))
+            check(fn(self.h, layer, _ptr(out), _stream(stream)))
+            if stream is not None:
+                cur = torch.cuda.current_stream(self.device)
+                if cur != stream:
+                    cur.wait_stream(stream)
+                    out.record_stream(stream)
         return out
 
+    def read_grad_shard(self, layer: int, stream=None) -> torch.Tensor:
+        return self._read_shard(lib().odc_read_grad_shard, layer, stream)
+
     def read_master_shard(self, layer: int, stream=None) -> torch.Tensor:
-        _, n = self.shard_range(layer)
-        out = torch.empty(max(n, 1), dtype=torch.float32, device=f"cuda:{self.device}")[:n]
-        if n:
-            check(lib().odc_read_master_shard(self.h, layer, _ptr(out), _stream(stream)))
-        return out
+        return self._read_shard(lib().odc_read_master_shard, layer, stream)
 
     def check(self, stream=None):
         """Synchronise `stream`; raise BarrierTimeout if the watchdog fired,
