@@ -549,11 +549,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int kvh = it.kv_head;
     const int G = g.H / g.KV;
     const int n_q = (it.seq_len + BQ - 1) / BQ;
-    // Iteration idx of the causal loop (G x (n_q - j) of them) is query tile i = n_q - 1 - idx / G
-    // (descending) and group head idx % G. Every CTA starts at the sequence's LAST query tile and
-    // walks down in step with the others, so at any time all CTAs of a sequence read Q / dO and
-    // add dQ rows of the same few query tiles: the fp32 dQ accumulator's working set stays in L2
-    // (ascending per-CTA loops spread it over the whole sequence, 201 MB at 32K x 12 heads).
+    const int per_head = n_q - j;  // query tiles i = j .. n_q-1 for each head of the group
     const int n0 = it.it_begin;
     const int n_iter = it.it_end - it.it_begin;
 
@@ -602,7 +598,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tma_2d(&map_v, &kv_full, sV, kvh * HD, k0);
             tma_2d(&map_v, &kv_full, sV + kTile / 2, kvh * HD + 64, k0);
             for (int n = 0; n < n_iter; ++n) {
-                const int h = kvh * G + (n0 + n) % G, i = n_q - 1 - (n0 + n) / G;
+                const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
                 const int q0 = it.seq_start + i * BQ, b = n & 1;
                 if (n >= 2) mbar_wait(&q_empty[b], ((n >> 1) - 1) & 1);  // Q_{n-2} consumed by dK_{n-2}
                 mbar_expect_tx(&q_full[b], kTile);
@@ -680,7 +676,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
         const float sl2 = g.scale_log2, sc = g.scale;
         auto stats = [&](int n, float& lse_raw, float& d_raw) {  // row statistics of iteration n (prefetched)
-            const int h = kvh * G + (n0 + n) % G, i = n_q - 1 - (n0 + n) / G;
+            const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
             const int qi = i * BQ + r;
             const long long idx = static_cast<long long>(h) * g.T + it.seq_start + qi;
             const bool ok = n < n_iter && qi < it.seq_len;
@@ -690,7 +686,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         float lse_nx, d_nx;
         stats(0, lse_nx, d_nx);
         for (int n = 0; n < n_iter; ++n) {
-            const int h = kvh * G + (n0 + n) % G, i = n_q - 1 - (n0 + n) / G;
+            const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
             const int qi = i * BQ + r;  // query index within the sequence
             const bool q_ok = qi < it.seq_len;
             const float lse2 = lse_nx * kLog2e;

@@ -109,7 +109,7 @@ def attn_fwd(q, k, v, items, scale):
 
 def attn_bwd_items(lens, H: int, KV: int, device, sms: int = 148) -> torch.Tensor:
     """Backward work list: per (sequence, 128-key tile, kv head) the causal loop
-    over (query tile >= key tile, descending; query head of the GQA group). Loops longer
+    over (query head of the GQA group, query tile >= key tile). Loops longer
     than ~1/(2*SMs) of the total are cut into chunks (their dK/dV partials meet
     in fp32 accumulators) so the grid load-balances; largest first (LPT)."""
     G = H // KV

@@ -116,16 +116,17 @@ def test_param_cache_matches_refetch():
         eng.minibatch_end()
         eng.check()
         grads.append([eng.read_grad_shard(u).clone() for u in range(len(sizes))])
-    # the glue kernels reduce with atomics (dw, bias grads, split-K), so two
-    # runs agree to fp32 rounding, not bitwise
+    # the glue and attention kernels reduce with atomics (dw, bias grads, split-K, dQ/dK/dV), so two
+    # runs agree up to the reduction order (and the bf16 roundings it can flip), not bitwise
     for a, b in zip(*grads):
-        torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-7)
+        rel = ((a - b).norm() / a.norm()).item()
+        assert rel < 2e-3 and torch.nn.functional.cosine_similarity(a, b, dim=0).item() > 0.99999, rel
 
 
 def test_recompute_matches_stored_activations():
     """Activation recompute re-runs the same kernels on the same fetched unit,
-    so the gradients must match the stored-activation path to fp32 rounding of
-    the atomically reduced parts."""
+    so the gradients must match the stored-activation path up to the
+    run-to-run order of the atomically reduced parts."""
     s = TINY_LLAMA
     sizes = W.unit_sizes(s)
     gen = torch.Generator(device=DEV).manual_seed(3)
@@ -142,9 +143,15 @@ def test_recompute_matches_stored_activations():
         eng.check()
         grads.append([eng.read_grad_shard(u).clone() for u in range(len(sizes))])
     assert max(losses) - min(losses) <= 1e-5 * abs(losses[0]), losses  # CE sums its chunks with atomics
+    # The recomputed paths run the same kernels on the same inputs, but the attention backward adds
+    # its fp32 dQ / dK / dV partials in a run-dependent order, and a 1-ulp fp32 difference that flips
+    # a bf16 rounding of dq/dk/dv moves single gradient elements by ~2^-8 relative. Compare each
+    # unit norm-wise (a real recompute bug — a wrong saved tensor, a stale buffer — is O(1) here).
     for g in grads[1:]:
         for a, b in zip(grads[0], g):
-            torch.testing.assert_close(a, b, rtol=1e-3, atol=1e-5)
+            rel = ((a - b).norm() / a.norm()).item()
+            cos = torch.nn.functional.cosine_similarity(a, b, dim=0).item()
+            assert rel < 2e-3 and cos > 0.99999, (rel, cos)
 
 
 def test_trace_schema_and_idle_fraction():
