@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -198,6 +199,11 @@ __device__ __forceinline__ void commit(unsigned long long* bar) {
         "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]),           \
         "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                                     \
         : "memory")
+
+#define TM_ST8(taddr, r)                                                                                     \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]), \
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])                     \
+                 : "memory")
 
 struct Item {
     int seq_start, seq_len, q_tile, head;
@@ -805,6 +811,391 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
+// ----------------------------------------------------------------------
+// Backward, transposed-score schedule. Same work items and outputs as
+// attn_bwd_kernel, but the scores are computed key-major, S^T = K_j Q_i^T
+// and dP^T = V_j dO_i^T (TMEM lane = key row), so that:
+//   - P^T (bf16) is written back into the S^T columns with tcgen05.st and is
+//     the TMEM A operand of dV += P^T dO (no smem round trip for P);
+//   - the elementwise work splits into phase A (P from S^T, as soon as S^T is
+//     ready) and phase B (dS from dP^T), and the tensor pipe always has work
+//     queued behind each phase. Tensor order per iteration n:
+//        dP^T_n | dV_n (needs A_n) | dQ_n (needs B_n) | S^T_{n+1} | dK_n
+//     phase A_{n+1} runs under dK_n and dP^T_{n+1}; phase B_n under dV_n;
+//     the dQ_n read-out under S^T_{n+1} and dK_n.
+//   - dQ_n = dS K_j (A = dS^T read MN-major from smem) goes to the dP^T
+//     columns; each warpgroup stages its 64 fp32 columns through one 32 KB
+//     buffer in turn (the other's TMA reduction read it first).
+// smem: K, V, Q x2, dO, dS^T, dQ staging (7 x 32 KB) + per-column lse / D.
+// TMEM: dV [0,128) dK [128,256) S^T/P^T [256,384) dP^T/dQ [384,512).
+constexpr int kBwd4Smem = kTile * 7 + 1024 + 1024;
+#ifndef ODC_BWD_POLY_EXP
+#define ODC_BWD_POLY_EXP 1
+#endif
+
+#ifdef ODC_ATTN_TRACE
+// per-iteration SM clock stamps of CTA 0 (tools/attn_bwd_trace.py): [event][iteration]
+constexpr int kTrEvents = 18, kTrIters = 64;
+__device__ unsigned long long g_attn_trace[kTrEvents * kTrIters];
+#define TR(ev, n)                                                                                  \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && (n) < kTrIters) g_attn_trace[(ev) * kTrIters + (n)] = clock64();    \
+    } while (0)
+#else
+#define TR(ev, n) \
+    do {          \
+    } while (0)
+#endif
+
+__device__ __forceinline__ void bar_wg(int w) {  // named barrier over one elementwise warpgroup
+    asm volatile("bar.sync %0, 128;" ::"r"(2 + w) : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_t_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                      const __grid_constant__ CUtensorMap map_dq, const __grid_constant__ CUtensorMap map_dk,
+                      const __grid_constant__ CUtensorMap map_dv, BwdArgs g) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    char* sK = smem;
+    char* sV = smem + kTile;
+    char* sQ0 = smem + 2 * kTile;  // Q double-buffered: S^T_{n+1} is issued before dK_n has read Q_n
+    char* sdO = smem + 4 * kTile;
+    char* sdS = smem + 5 * kTile;  // dS^T [key][query], K-major for dK, MN-major for dQ
+    char* sStage = smem + 6 * kTile;
+    float* sCol = reinterpret_cast<float*>(smem + 7 * kTile);  // [wg][lse2 64 | Ds 64]
+    // s_full: S^T_n in TMEM; dp_full: dP^T_n in TMEM; p_full: P^T_n in TMEM (S^T_n read);
+    // ds_full: dS^T_n in smem (dP^T_n read); dq_full: dQ_n in TMEM; dq_read: dQ_n read out;
+    // stg_free[w]: the staging buffer may be written by warpgroup w; mma_done: every MMA finished
+    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, s_full, dp_full,
+        p_full, ds_full, dq_full, dq_read, stg_free[2], mma_done;
+    __shared__ unsigned tmem_base;
+
+    const BwdItem it = g.items[blockIdx.x];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int j = it.kv_tile;
+    const int kvh = it.kv_head;
+    const int G = g.H / g.KV;
+    const int n_q = (it.seq_len + BQ - 1) / BQ;
+    const int per_head = n_q - j;
+    const int n0 = it.it_begin;
+    const int n_iter = it.it_end - it.it_begin;
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(&kv_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&q_full[b], 1);
+            mbar_init(&q_empty[b], 1);
+            mbar_init(&stg_free[b], 1);
+        }
+        mbar_init(&do_full, 1);
+        mbar_init(&do_empty, 1);
+        mbar_init(&s_full, 1);
+        mbar_init(&dp_full, 1);
+        mbar_init(&p_full, 8);
+        mbar_init(&ds_full, 8);
+        mbar_init(&dq_full, 1);
+        mbar_init(&dq_read, 8);
+        mbar_init(&mma_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base;
+    const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;
+
+    if (warp < 4) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+      if (warp == 0) {
+        if (lane == 0) {  // ---- TMA
+            const int k0 = it.seq_start + j * BKV;
+            mbar_expect_tx(&kv_full, 2 * kTile);
+            tma_2d(&map_k, &kv_full, sK, kvh * HD, k0);
+            tma_2d(&map_k, &kv_full, sK + kTile / 2, kvh * HD + 64, k0);
+            tma_2d(&map_v, &kv_full, sV, kvh * HD, k0);
+            tma_2d(&map_v, &kv_full, sV + kTile / 2, kvh * HD + 64, k0);
+            for (int n = 0; n < n_iter; ++n) {
+                const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
+                const int q0 = it.seq_start + i * BQ, b = n & 1;
+                if (n >= 2) mbar_wait(&q_empty[b], ((n >> 1) - 1) & 1);  // Q_{n-2} consumed by dK_{n-2}
+                mbar_expect_tx(&q_full[b], kTile);
+                tma_2d(&map_q, &q_full[b], sQ0 + b * kTile, h * HD, q0);
+                tma_2d(&map_q, &q_full[b], sQ0 + b * kTile + kTile / 2, h * HD + 64, q0);
+                if (n >= 1) mbar_wait(&do_empty, (n - 1) & 1);  // dO_{n-1} consumed by dV_{n-1}
+                mbar_expect_tx(&do_full, kTile);
+                tma_2d(&map_do, &do_full, sdO, h * HD, q0);
+                tma_2d(&map_do, &do_full, sdO + kTile / 2, h * HD + 64, q0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const unsigned id_kk = instr(0, 0), id_mm = instr(1, 1), id_km = instr(0, 1);
+            mbar_wait(&kv_full, 0);
+            const unsigned doa = su32(sdO), ka = su32(sK), va = su32(sV), dsa = su32(sdS);
+            auto issue_st = [&](int n) {  // S^T_n = K Q_n^T
+                const unsigned qa = su32(sQ0 + (n & 1) * kTile);
+                mbar_wait(&q_full[n & 1], (n >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + T_S, sdesc(ka + off, 16, 1024), sdesc(qa + off, 16, 1024), id_kk, kk > 0);
+                }
+                commit(&s_full);
+            };
+            issue_st(0);
+            for (int n = 0; n < n_iter; ++n) {
+                const unsigned qa = su32(sQ0 + (n & 1) * kTile);
+                mbar_wait(&do_full, n & 1);
+                if (n > 0) mbar_wait(&dq_read, (n - 1) & 1);  // dQ_{n-1} read out: dP^T columns free
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TR(0, n);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {  // dP^T = V dO^T
+                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + T_DP, sdesc(va + off, 16, 1024), sdesc(doa + off, 16, 1024), id_kk, kk > 0);
+                }
+                commit(&dp_full);
+                mbar_wait(&p_full, n & 1);  // P^T_n (bf16) over the first 32 columns of each 64-column half
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TR(1, n);
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO: A from TMEM, B = dO MN-major
+                    mma_ts(tmem + T_DV, tmem + T_S + (kk >> 2) * 64 + (kk & 3) * 8,
+                           sdesc(doa + kk * 2048, kTile / 2, 1024), id_km, (n > 0 || kk > 0));
+                commit(&do_empty);
+                mbar_wait(&ds_full, n & 1);  // dS^T_n in smem
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TR(2, n);
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk)  // dQ = dS K: A = dS^T read MN-major, B = K MN-major
+                    mma(tmem + T_DP, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024),
+                        id_mm, kk > 0);
+                commit(&dq_full);
+                if (n + 1 < n_iter) issue_st(n + 1);  // in order after dV_n, which read P^T_n from these columns
+                TR(3, n);
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk) {  // dK += dS^T Q: A = dS^T K-major, B = Q MN-major
+                    const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                    mma(tmem + T_DK, sdesc(dsa + aoff, 16, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024), id_km,
+                        (n > 0 || kk > 0));
+                }
+                commit(&q_empty[n & 1]);
+                TR(4, n);
+            }
+            commit(&mma_done);
+        }
+      }
+    } else {  // ---- elementwise: key row r of the tile, query columns [c0, c0 + 64); dQ read-out: query row r
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+        const int quad = warp % 4;
+        const int w = (warp - 4) >> 2;
+        const int c0 = w * 64;
+        const bool lead = quad == 0 && lane == 0;  // issues this warpgroup's TMA reductions
+        const int r = quad * 32 + lane;
+        const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
+        const float sl2 = g.scale_log2, sc = g.scale;
+        float* col = sCol + w * 128;  // lse2 [64] | Ds [64] of this warpgroup's query columns
+        const int kr = j * BKV + r;   // key index within the sequence
+        auto col_stat = [&](int n) {  // thread r < 64: lse of column r; r >= 64: D of column r - 64
+            if (n >= n_iter) return 0.f;
+            const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
+            const int qi = i * BQ + c0 + (r & 63);
+            if (qi >= it.seq_len) return 0.f;
+            const long long idx = static_cast<long long>(h) * g.T + it.seq_start + qi;
+            return r < 64 ? __ldg(g.lse + idx) * kLog2e : __ldg(g.D + idx) * sc;
+        };
+        float stat_nx = col_stat(0);
+        // The staging buffer carries wg0's dQ_n, then wg1's dQ_n, then wg0's dQ_{n+1}, ... Each lead
+        // waits for its reduction to have read the buffer only later (after its next phase A / B), so
+        // the drain overlaps the elementwise work; wg1 keeps dQ_n in registers over phase A_{n+1}.
+        unsigned v[64];
+        int dq_col = 0, dq_row = 0;  // wg1: where its held dQ goes
+        auto reduce_dq = [&](int col0, int row0) {
+            stage_f32(sStage, r, 0, v);  // query rows past the sequence end hold exact zeros
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_wg(w);
+            if (lead) {
+                tma_reduce_add(&map_dq, sStage, col0, row0);
+                tma_reduce_add(&map_dq, sStage + kTile / 2, col0 + 32, row0);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        };
+        for (int n = 0; n < n_iter; ++n) {
+            const int h = kvh * G + (n0 + n) / per_head, i = j + (n0 + n) % per_head;
+            col[r] = stat_nx;  // every reader of the previous values passed this warpgroup's last barrier
+            stat_nx = col_stat(n + 1);
+            bar_wg(w);
+            const int qbase = i * BQ + c0;
+            const int lo = kr - qbase;              // columns x < lo: query before the key (causal)
+            const int hi = it.seq_len - qbase;      // columns x >= hi: past the sequence end
+            // ---- phase A: P^T = exp2(S^T * scale*log2e - lse2[q])
+            mbar_wait(&s_full, n & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lead) TR(5 + 8 * w, n);
+            unsigned p[64];
+            TM_LD32(tmem + lane_base + T_S + c0, p);
+            TM_LD32(tmem + lane_base + T_S + c0 + 32, (p + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const float2 v_sl2 = make_float2(sl2, sl2);
+            if (lo <= 0 && hi >= 64) {
+#pragma unroll
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 ls = *reinterpret_cast<const float2*>(col + x);
+                    const float2 t = ffma2(make_float2(__uint_as_float(p[x]), __uint_as_float(p[x + 1])), v_sl2,
+                                           make_float2(-ls.x, -ls.y));
+                    if (ODC_BWD_POLY_EXP && (x & 2)) {  // every other pair on the FMA pipe: MUFU.EX2 is 16/clk/SM
+                        const float2 e = ex2_fma2(t);
+                        p[x] = __float_as_uint(e.x);
+                        p[x + 1] = __float_as_uint(e.y);
+                    } else {
+                        p[x] = __float_as_uint(ex2(t.x));
+                        p[x + 1] = __float_as_uint(ex2(t.y));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 ls = *reinterpret_cast<const float2*>(col + x);
+                    const float2 t = ffma2(make_float2(__uint_as_float(p[x]), __uint_as_float(p[x + 1])), v_sl2,
+                                           make_float2(-ls.x, -ls.y));
+                    p[x] = __float_as_uint((x < lo || x >= hi) ? 0.f : ex2(t.x));
+                    p[x + 1] = __float_as_uint((x + 1 < lo || x + 1 >= hi) ? 0.f : ex2(t.y));
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // bf16 pairs over the first 32 of this warpgroup's 64 S^T columns
+                unsigned pk[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                    pk[x] = pack_bf16(__uint_as_float(p[16 * c + 2 * x]), __uint_as_float(p[16 * c + 2 * x + 1]));
+                TM_ST8(tmem + lane_base + T_S + c0 + 8 * c, pk);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full);
+            if (lead && w == 0) TR(6, n);
+            if (n > 0) {
+                if (w == 0) {
+                    if (lead) {  // wg0's dQ_{n-1} read out of the buffer: wg1 may stage
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        mbar_arrive(&stg_free[1]);
+                        TR(12, n);
+                    }
+                } else {
+                    mbar_wait(&stg_free[1], (n - 1) & 1);
+                    if (lead) TR(16, n);
+                    reduce_dq(dq_col, dq_row);
+                }
+            }
+            // ---- phase B: dS^T = P^T * (dP^T * scale - D * scale) -> smem
+            mbar_wait(&dp_full, n & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lead) TR(7 + 7 * w, n);
+            {
+                unsigned dp[64];
+                TM_LD32(tmem + lane_base + T_DP + c0, dp);
+                TM_LD32(tmem + lane_base + T_DP + c0 + 32, (dp + 32));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const float2 v_sc = make_float2(sc, sc);
+#pragma unroll
+                for (int x = 0; x < 64; x += 2) {
+                    const float2 ds = *reinterpret_cast<const float2*>(col + 64 + x);
+                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc,
+                                           make_float2(-ds.x, -ds.y));
+                    const float2 d = fmul2(make_float2(__uint_as_float(p[x]), __uint_as_float(p[x + 1])), u);
+                    dp[x / 2] = pack_bf16(d.x, d.y);
+                }
+                store_swizzled(sdS, r, c0, dp);
+                store_swizzled(sdS, r, c0 + 32, dp + 16);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ds_full);
+            if (lead && w == 0) TR(8, n);
+            if (n > 0 && w == 1 && lead) {  // wg1's dQ_{n-1} read out: wg0 may stage dQ_n
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(&stg_free[0]);
+                TR(17, n);
+            }
+            // ---- dQ_n (query row r, columns [c0, c0+64)) -> staging -> TMA reduce-add
+            mbar_wait(&dq_full, n & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lead) TR(9 + 6 * w, n);
+            TM_LD32(tmem + lane_base + T_DP + c0, v);
+            TM_LD32(tmem + lane_base + T_DP + c0 + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dq_read);
+            if (lead && w == 0) TR(10, n);
+            dq_col = h * HD + c0;
+            dq_row = it.seq_start + i * BQ;
+            if (w == 0) {
+                if (n > 0) mbar_wait(&stg_free[0], (n - 1) & 1);
+                if (lead) TR(11, n);
+                reduce_dq(dq_col, dq_row);
+            }
+        }
+        // the last dQ: wg0's drains, then wg1 stages its held one
+        if (w == 0) {
+            if (lead) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(&stg_free[1]);
+            }
+        } else {
+            mbar_wait(&stg_free[1], (n_iter - 1) & 1);
+            reduce_dq(dq_col, dq_row);
+            if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        // dK, dV of the key tile -> staging (Q x2 for dK; dO, dS^T for dV) -> TMA reduce-add
+        mbar_wait(&mma_done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        bar_ew();  // both warpgroups' dQ reductions have read the staging buffer
+        char* st_dv = sdO;  // [sdO, sdS]
+        char* st_dk = sQ0;
+        {
+            unsigned v[64];
+            TM_LD32(tmem + lane_base + T_DV + c0, v);
+            TM_LD32(tmem + lane_base + T_DV + c0 + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            stage_f32(st_dv, r, c0, v);
+            TM_LD32(tmem + lane_base + T_DK + c0, v);
+            TM_LD32(tmem + lane_base + T_DK + c0 + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            stage_f32(st_dk, r, c0, v);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_ew();
+        if (warp == 4 && lane == 0) {
+            const int krow0 = it.seq_start + j * BKV;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                tma_reduce_add(&map_dv, st_dv + k * (kTile / 2), kvh * HD + 32 * k, krow0);
+                tma_reduce_add(&map_dk, st_dk + k * (kTile / 2), kvh * HD + 32 * k, krow0);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        if (lead && w == 1) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 // D[h][t] = sum_c dO[t][h][c] * O[t][h][c]; one warp per (t, h) row; also zeroes dq_acc rows
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ D, float* __restrict__ dq_acc, long long T, int H) {
@@ -994,10 +1385,16 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
         if (head_dim != HD) throw odcsim::ParamError("attn_bwd: head_dim must be 128");
         if (KV < 1 || H % KV) throw odcsim::ParamError("attn_bwd: H must be a multiple of KV");
         static thread_local int configured = -1;
+        static const bool use_t = [] {  // A/B while the transposed schedule is tuned
+            const char* e = std::getenv("ODC_ATTN_BWD");
+            return e && std::strcmp(e, "t") == 0;
+        }();
         int dev = 0;
         cudaGetDevice(&dev);
         if (configured != dev) {
             cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(attn_bwd_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwd4Smem);
             if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
@@ -1034,7 +1431,10 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
             a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
-            attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
+            if (use_t)
+                attn_bwd_t_kernel<<<n_items, kBwdThreads, kBwd4Smem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
+            else
+                attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
         *dq_out = dq_acc;
         *dk_out = dk_acc;
@@ -1042,6 +1442,12 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
     }
 }
 }  // namespace
+
+#ifdef ODC_ATTN_TRACE
+extern "C" int odc_attn_trace_read(unsigned long long* dst) {
+    return cudaMemcpyFromSymbol(dst, odc::attn::g_attn_trace, sizeof(odc::attn::g_attn_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
                                    const float* lse, void* dq, void* dk, void* dv, void* workspace,
