@@ -1,5 +1,5 @@
 """Per-iteration timeline of the transposed-score attention backward
-(attn_bwd_t_kernel) in CTA 0, from SM clock stamps recorded by the
+(attn_bwd_t_kernel, specialised warpgroups) in CTA 0, from SM clock stamps recorded by the
 ODC_ATTN_TRACE build (`python -m paper_2601_19362_b200.build --variant trace
 ODC_ATTN_TRACE`). Prints each event's median offset (SM cycles) from the
 iteration's dP^T issue, and the median iteration period.
@@ -18,10 +18,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_19362_b200 import fused as F  # noqa: E402
 from paper_2601_19362_b200._lib import lib  # noqa: E402
 
-EV = ["mma:dP_issue", "mma:dV_issue(p_full)", "mma:dQ_issue(ds_full)", "mma:S_next_issued", "mma:dK_issued",
-      "wg0:A_start(s_full)", "wg0:A_end", "wg0:B_start(dp_full)", "wg0:B_end", "wg0:dQ_start(dq_full)",
-      "wg0:dq_read", "wg0:stage_start", "wg0:prev_dQ_drained", "wg1:A_start", "wg1:B_start", "wg1:dQ_start",
-      "wg1:stage_prev_start", "wg1:prev_dQ_drained"]
+EV = ["mma:dP_issue", "mma:dV_issue(p_full)", "mma:S_next_issue(p_read)", "mma:dQ_issue(ds_full)",
+      "mma:dK_issued", "A:start(s_full)", "A:end(p_full)", "B:start(dp_full,p_full)", "B:p_read",
+      "B:end(ds_full)", "B:dQ_start(dq_full)", "B:dq_read", "B:sent_to_peer", "B:peer_half_added", "B:dQ_reduce_issued",
+      "B:prev_dQ_drained"]
 NI = 64
 
 lens, H, KV = [int(x) for x in os.environ.get("LENS", "32768").split(",")], 12, 2
