@@ -26,7 +26,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -199,11 +198,6 @@ __device__ __forceinline__ void commit(unsigned long long* bar) {
         "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]),           \
         "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                                     \
         : "memory")
-
-#define TM_ST8(taddr, r)                                                                                     \
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]), \
-                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])                     \
-                 : "memory")
 
 struct Item {
     int seq_start, seq_len, q_tile, head;
@@ -811,456 +805,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
-// ----------------------------------------------------------------------
-// Backward, transposed-score schedule with specialised elementwise
-// warpgroups. Same work items and outputs as attn_bwd_kernel, but the scores
-// are computed key-major, S^T = K_j Q_i^T and dP^T = V_j dO_i^T (TMEM lane =
-// key row), so that P^T (bf16) is written back over the S^T columns with
-// tcgen05.st and is the TMEM A operand of dV += P^T dO (no smem round trip).
-//   warpgroup A (warps 4-7): P^T_n = exp2(S^T_n*scale*log2e - lse2[q]) for
-//       all 128 query columns (half of the exp2 on the FMA pipe: MUFU.EX2 is
-//       16/clk/SM, profiles/r02/pipe_probe.txt)
-//   warpgroup B (warps 8-11): dS^T_n = P^T_n * (dP^T_n*scale - D*scale) from
-//       the bf16 P^T in TMEM -> smem, then the dQ_n read-out and its two
-//       32 KB stagings (the spare buffer, and the dS^T buffer once dK_n has
-//       read it) -> TMA reduce-add into the fp32 dQ accumulator.
-// Tensor order per iteration n (one elected thread):
-//   dP^T_n | dV_n (needs A_n) | S^T_{n+1} (needs B_n to have read P^T_n) |
-//   dQ_n (needs B_n) | dK_n
-// so A_{n+1} runs under dQ_n, dK_n, dP^T_{n+1}; B_n under dV_n, S^T_{n+1};
-// the dQ read-out under dK_n.
-// dQ traffic: CTA pairs (a cluster of 2) own adjacent key tiles 2p, 2p+1 and walk
-// the same (head, query tile) loop in lockstep; each sends the half of its dQ_n
-// partial the other owns into the other's staging buffer over DSMEM, adds the
-// received half to its own and reduces 32 KB instead of 64 KB into L2 (the L2
-// reduction drains ~20 B/clk/SM: profiles/r02/attn_bwd_t/).
-// smem: K, V, Q x2, dO, dS^T, dQ exchange/staging (7 x 32 KB) + per-column lse / D (x2).
-// TMEM: dV [0,128) dK [128,256) S^T/P^T [256,384) dP^T/dQ [384,512).
-constexpr int kBwd4Smem = kTile * 7 + 2048;  // the 1024-aligned dynamic base needs no slack (checked)
-#ifndef ODC_BWD_POLY_EXP
-#define ODC_BWD_POLY_EXP 1
-#endif
-
-#ifdef ODC_ATTN_TRACE
-// per-iteration SM clock stamps of CTA 0 (tools/attn_bwd_trace.py): [event][iteration]
-constexpr int kTrEvents = 16, kTrIters = 64;
-__device__ unsigned long long g_attn_trace[kTrEvents * kTrIters];
-#define TR(ev, n)                                                                                  \
-    do {                                                                                           \
-        if (blockIdx.x == 0 && (n) < kTrIters) g_attn_trace[(ev) * kTrIters + (n)] = clock64();    \
-    } while (0)
-#else
-#define TR(ev, n) \
-    do {          \
-    } while (0)
-#endif
-
-__device__ __forceinline__ void bar_wg(int w) {  // named barrier over one elementwise warpgroup
-    asm volatile("bar.sync %0, 128;" ::"r"(2 + w) : "memory");
-}
-__device__ __forceinline__ unsigned mapa_peer(unsigned a, unsigned rank) {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(unsigned remote_bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity) {
-    asm volatile(
-        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
-            su32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void st_cluster128(unsigned a, unsigned x, unsigned y, unsigned z, unsigned w) {
-    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
-    attn_bwd_t_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
-                      const __grid_constant__ CUtensorMap map_dq, const __grid_constant__ CUtensorMap map_dk,
-                      const __grid_constant__ CUtensorMap map_dv, BwdArgs g) {
-    extern __shared__ __align__(1024) char smem_raw[];
-    if (su32(smem_raw) & 1023) __trap();  // kBwd4Smem has no alignment slack
-    char* smem = smem_raw;
-    char* sK = smem;
-    char* sV = smem + kTile;
-    char* sQ0 = smem + 2 * kTile;  // Q double-buffered: S^T_{n+1} is issued before dK_n has read Q_n
-    char* sdO = smem + 4 * kTile;
-    char* sdS = smem + 5 * kTile;  // dS^T [key][query]: K-major A of dK, MN-major A of dQ; then dQ staging
-    char* sStage = smem + 6 * kTile;
-    float* sCol = reinterpret_cast<float*>(smem + 7 * kTile);  // lse2 [2][128] (A) | Ds [2][128] (B)
-    // s_full: S^T_n in TMEM; p_full: P^T_n in TMEM; p_read: B has P^T_n in registers (columns free for
-    // S^T_{n+1}); dp_full: dP^T_n in TMEM; ds_full: dS^T_n in smem, dP^T_n read; dq_full: dQ_n in TMEM;
-    // dq_read: dQ_n read out; dk_done: dK_n finished; mma_done: every MMA finished;
-    // recv_full: the peer's half of dQ_n is in sStage; peer_free: the peer's sStage may be written
-    __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, s_full, p_full,
-        p_read, dp_full, ds_full, dq_full, dq_read, dk_done, mma_done, recv_full, peer_free;
-    __shared__ unsigned tmem_base;
-
-    unsigned rank;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    const BwdItem it = g.items[blockIdx.x >> 1];  // one item per CTA pair
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int jp = it.kv_tile;                   // the pair's first key tile: the query loop is i >= jp for both
-    const int j = jp + static_cast<int>(rank);  // this CTA's key tile (past the sequence end: all masked)
-    const int kvh = it.kv_head;
-    const int G = g.H / g.KV;
-    const int n_q = (it.seq_len + BQ - 1) / BQ;
-    const int per_head = n_q - jp;
-    const int n0 = it.it_begin;
-    const int n_iter = it.it_end - it.it_begin;
-
-    if (warp == 0 && lane == 0) {
-        mbar_init(&kv_full, 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&q_full[b], 1);
-            mbar_init(&q_empty[b], 1);
-        }
-        mbar_init(&do_full, 1);
-        mbar_init(&do_empty, 1);
-        mbar_init(&s_full, 1);
-        mbar_init(&p_full, 4);
-        mbar_init(&p_read, 4);
-        mbar_init(&dp_full, 1);
-        mbar_init(&ds_full, 4);
-        mbar_init(&dq_full, 1);
-        mbar_init(&dq_read, 4);
-        mbar_init(&dk_done, 1);
-        mbar_init(&mma_done, 1);
-        mbar_init(&recv_full, 128);
-        mbar_init(&peer_free, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const unsigned tmem = tmem_base;
-    const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;
-
-    if (warp < 4) {
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
-      if (warp == 0) {
-        if (lane == 0) {  // ---- TMA
-            const int k0 = it.seq_start + j * BKV;
-            mbar_expect_tx(&kv_full, 2 * kTile);
-            tma_2d(&map_k, &kv_full, sK, kvh * HD, k0);
-            tma_2d(&map_k, &kv_full, sK + kTile / 2, kvh * HD + 64, k0);
-            tma_2d(&map_v, &kv_full, sV, kvh * HD, k0);
-            tma_2d(&map_v, &kv_full, sV + kTile / 2, kvh * HD + 64, k0);
-            for (int n = 0; n < n_iter; ++n) {
-                const int h = kvh * G + (n0 + n) / per_head, i = jp + (n0 + n) % per_head;
-                const int q0 = it.seq_start + i * BQ, b = n & 1;
-                if (n >= 2) mbar_wait(&q_empty[b], ((n >> 1) - 1) & 1);  // Q_{n-2} consumed by dK_{n-2}
-                mbar_expect_tx(&q_full[b], kTile);
-                tma_2d(&map_q, &q_full[b], sQ0 + b * kTile, h * HD, q0);
-                tma_2d(&map_q, &q_full[b], sQ0 + b * kTile + kTile / 2, h * HD + 64, q0);
-                if (n >= 1) mbar_wait(&do_empty, (n - 1) & 1);  // dO_{n-1} consumed by dV_{n-1}
-                mbar_expect_tx(&do_full, kTile);
-                tma_2d(&map_do, &do_full, sdO, h * HD, q0);
-                tma_2d(&map_do, &do_full, sdO + kTile / 2, h * HD + 64, q0);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
-            const unsigned id_kk = instr(0, 0), id_mm = instr(1, 1), id_km = instr(0, 1);
-            mbar_wait(&kv_full, 0);
-            const unsigned doa = su32(sdO), ka = su32(sK), va = su32(sV), dsa = su32(sdS);
-            auto issue_st = [&](int n) {  // S^T_n = K Q_n^T
-                const unsigned qa = su32(sQ0 + (n & 1) * kTile);
-                mbar_wait(&q_full[n & 1], (n >> 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                    mma(tmem + T_S, sdesc(ka + off, 16, 1024), sdesc(qa + off, 16, 1024), id_kk, kk > 0);
-                }
-                commit(&s_full);
-            };
-            issue_st(0);
-            for (int n = 0; n < n_iter; ++n) {
-                const unsigned qa = su32(sQ0 + (n & 1) * kTile);
-                mbar_wait(&do_full, n & 1);
-                if (n > 0) mbar_wait(&dq_read, (n - 1) & 1);  // dQ_{n-1} read out: dP^T columns free
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                TR(0, n);
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {  // dP^T = V dO^T
-                    const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                    mma(tmem + T_DP, sdesc(va + off, 16, 1024), sdesc(doa + off, 16, 1024), id_kk, kk > 0);
-                }
-                commit(&dp_full);
-                mbar_wait(&p_full, n & 1);  // P^T_n: bf16 pairs over S^T columns [0, 64)
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                TR(1, n);
-#pragma unroll
-                for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO: A from TMEM, B = dO MN-major
-                    mma_ts(tmem + T_DV, tmem + T_S + kk * 8, sdesc(doa + kk * 2048, kTile / 2, 1024), id_km,
-                           (n > 0 || kk > 0));
-                commit(&do_empty);
-                if (n + 1 < n_iter) {  // S^T_{n+1} over P^T_n: after dV_n (in order) and B's read of P^T_n
-                    mbar_wait(&p_read, n & 1);
-                    TR(2, n);
-                    issue_st(n + 1);
-                }
-                mbar_wait(&ds_full, n & 1);  // dS^T_n in smem
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                TR(3, n);
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)  // dQ = dS K: A = dS^T read MN-major, B = K MN-major
-                    mma(tmem + T_DP, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024),
-                        id_mm, kk > 0);
-                commit(&dq_full);
-#pragma unroll
-                for (int kk = 0; kk < BQ / 16; ++kk) {  // dK += dS^T Q: A = dS^T K-major, B = Q MN-major
-                    const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                    mma(tmem + T_DK, sdesc(dsa + aoff, 16, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024), id_km,
-                        (n > 0 || kk > 0));
-                }
-                commit(&q_empty[n & 1]);
-                commit(&dk_done);
-                TR(4, n);
-            }
-            commit(&mma_done);
-        }
-      }
-    } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
-        const int quad = warp % 4;
-        const int w = (warp - 4) >> 2;  // 0: warpgroup A, 1: warpgroup B
-        const bool lead = quad == 0 && lane == 0;
-        const int r = quad * 32 + lane;  // key row (A, B) / query row (dQ read-out)
-        const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
-        const float sl2 = g.scale_log2, sc = g.scale;
-        float* col = sCol + w * 256;  // [2][128] per-column lse2 (A) or D*scale (B) of iterations n&1
-        auto col_stat = [&](int n) {  // thread r: the statistic of query column r of iteration n
-            if (n >= n_iter) return 0.f;
-            const int h = kvh * G + (n0 + n) / per_head, i = jp + (n0 + n) % per_head;
-            const int qi = i * BQ + r;
-            if (qi >= it.seq_len) return 0.f;
-            const long long idx = static_cast<long long>(h) * g.T + it.seq_start + qi;
-            return w == 0 ? __ldg(g.lse + idx) * kLog2e : __ldg(g.D + idx) * sc;
-        };
-        float stat_nx = col_stat(0);
-        if (w == 0) {  // ---------------- warpgroup A: P^T
-            const int kr = j * BKV + r;  // key index within the sequence
-            for (int n = 0; n < n_iter; ++n) {
-                const int i = jp + (n0 + n) % per_head;
-                float* ls = col + (n & 1) * 128;
-                ls[r] = stat_nx;  // the readers of this buffer (iteration n-2) passed the barrier of n-1
-                stat_nx = col_stat(n + 1);
-                bar_wg(0);
-                const int lo = kr - i * BQ;          // columns x < lo: query before the key (causal)
-                const int hi = it.seq_len - i * BQ;  // columns x >= hi: past the sequence end
-                mbar_wait(&s_full, n & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lead) TR(5, n);
-                const float2 v_sl2 = make_float2(sl2, sl2);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {  // 64 query columns per chunk
-                    unsigned p[64];
-                    TM_LD32(tmem + lane_base + T_S + 64 * c, p);
-                    TM_LD32(tmem + lane_base + T_S + 64 * c + 32, (p + 32));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    const int clo = lo - 64 * c, chi = hi - 64 * c;
-                    if (clo <= 0 && chi >= 64) {
-#pragma unroll
-                        for (int x = 0; x < 64; x += 2) {
-                            const float2 l2 = *reinterpret_cast<const float2*>(ls + 64 * c + x);
-                            const float2 t = ffma2(make_float2(__uint_as_float(p[x]), __uint_as_float(p[x + 1])), v_sl2,
-                                                   make_float2(-l2.x, -l2.y));
-                            float2 e;
-                            if (ODC_BWD_POLY_EXP && (x & 2)) {
-                                e = ex2_fma2(t);
-                            } else {
-                                e = make_float2(ex2(t.x), ex2(t.y));
-                            }
-                            p[x / 2] = pack_bf16(e.x, e.y);
-                        }
-                    } else {
-#pragma unroll
-                        for (int x = 0; x < 64; x += 2) {
-                            const float2 l2 = *reinterpret_cast<const float2*>(ls + 64 * c + x);
-                            const float2 t = ffma2(make_float2(__uint_as_float(p[x]), __uint_as_float(p[x + 1])), v_sl2,
-                                                   make_float2(-l2.x, -l2.y));
-                            p[x / 2] = pack_bf16((x < clo || x >= chi) ? 0.f : ex2(t.x),
-                                                 (x + 1 < clo || x + 1 >= chi) ? 0.f : ex2(t.y));
-                        }
-                    }
-                    // packed columns [32c, 32c+32): S^T columns already in registers (chunk 0's, or this chunk's)
-                    TM_ST32(tmem + lane_base + T_S + 32 * c, p);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&p_full);
-                if (lead) TR(6, n);
-            }
-        } else {  // ---------------- warpgroup B: dS^T, dQ
-            for (int n = 0; n < n_iter; ++n) {
-                const int h = kvh * G + (n0 + n) / per_head, i = jp + (n0 + n) % per_head;
-                float* dsc = col + (n & 1) * 128;
-                dsc[r] = stat_nx;
-                stat_nx = col_stat(n + 1);
-                bar_wg(1);
-                mbar_wait(&dp_full, n & 1);  // dP^T_n; P^T_n is complete too (dV_n... no: p_full) -> wait both
-                mbar_wait(&p_full, n & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lead) TR(7, n);
-                unsigned pk[64];  // P^T_n, bf16 pairs of the 128 query columns
-                TM_LD32(tmem + lane_base + T_S, pk);
-                TM_LD32(tmem + lane_base + T_S + 32, (pk + 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&p_read);
-                if (lead) TR(8, n);
-                const float2 v_sc = make_float2(sc, sc);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    unsigned dp[64];
-                    TM_LD32(tmem + lane_base + T_DP + 64 * c, dp);
-                    TM_LD32(tmem + lane_base + T_DP + 64 * c + 32, (dp + 32));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int x = 0; x < 64; x += 2) {
-                        const float2 ds = *reinterpret_cast<const float2*>(dsc + 64 * c + x);
-                        const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc,
-                                               make_float2(-ds.x, -ds.y));
-                        const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pk[32 * c + x / 2]);
-                        const float2 d = fmul2(__bfloat1622float2(pb), u);
-                        dp[x / 2] = pack_bf16(d.x, d.y);
-                    }
-                    store_swizzled(sdS, r, 64 * c, dp);
-                    store_swizzled(sdS, r, 64 * c + 32, dp + 16);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&ds_full);
-                if (lead) TR(9, n);
-                if (n > 0 && lead) {  // our reduction of dQ_{n-1} has read sStage: the peer may send dQ_n
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    mbar_arrive_remote(mapa_peer(su32(&peer_free), rank ^ 1));
-                    TR(15, n);
-                }
-                // ---- dQ_n (query row r): columns [0,64) via the spare buffer, [64,128) via the dS^T buffer
-                mbar_wait(&dq_full, n & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lead) TR(10, n);
-                unsigned v0[64], v1[64];
-                TM_LD32(tmem + lane_base + T_DP, v0);
-                TM_LD32(tmem + lane_base + T_DP + 32, (v0 + 32));
-                TM_LD32(tmem + lane_base + T_DP + 64, v1);
-                TM_LD32(tmem + lane_base + T_DP + 96, (v1 + 32));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&dq_read);
-                if (lead) TR(11, n);
-                // the pair exchange: this CTA owns dQ columns [64*rank, 64*rank + 64) of the pair's sum
-                auto send = [&](const unsigned(&x)[64]) {  // into the peer's sStage, staging layout
-                    if (n > 0) mbar_wait_cluster(&peer_free, (n - 1) & 1);
-                    const unsigned base = mapa_peer(su32(sStage), rank ^ 1);
-#pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        const unsigned row = base + k * (kTile / 2) + r * 128;
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            st_cluster128(row + ((q ^ (r & 7)) << 4), x[32 * k + 4 * q], x[32 * k + 4 * q + 1],
-                                          x[32 * k + 4 * q + 2], x[32 * k + 4 * q + 3]);
-                    }
-                    mbar_arrive_remote(mapa_peer(su32(&recv_full), rank ^ 1));
-                };
-                auto add_own = [&](const unsigned(&x)[64]) {  // received half + ours, in place
-                    mbar_wait_cluster(&recv_full, n & 1);
-#pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        char* row = sStage + k * (kTile / 2) + r * 128;
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            float4* p4 = reinterpret_cast<float4*>(row + ((q ^ (r & 7)) << 4));
-                            float4 a = *p4;
-                            a.x += __uint_as_float(x[32 * k + 4 * q]);
-                            a.y += __uint_as_float(x[32 * k + 4 * q + 1]);
-                            a.z += __uint_as_float(x[32 * k + 4 * q + 2]);
-                            a.w += __uint_as_float(x[32 * k + 4 * q + 3]);
-                            *p4 = a;
-                        }
-                    }
-                };
-                if (rank == 0) {
-                    send(v1);
-                    if (lead) TR(12, n);
-                    add_own(v0);
-                } else {
-                    send(v0);
-                    if (lead) TR(12, n);
-                    add_own(v1);
-                }
-                if (lead) TR(13, n);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bar_wg(1);
-                if (lead) {
-                    const int row0 = it.seq_start + i * BQ, col0 = h * HD + 64 * static_cast<int>(rank);
-                    tma_reduce_add(&map_dq, sStage, col0, row0);
-                    tma_reduce_add(&map_dq, sStage + kTile / 2, col0 + 32, row0);
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    TR(14, n);
-                }
-            }
-            if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-        // dK, dV of the key tile -> staging (Q x2 for dK; dO, dS^T for dV) -> TMA reduce-add
-        mbar_wait(&mma_done, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        bar_ew();  // and warpgroup B's dQ reductions have read the dS^T / spare buffers
-        const int c0 = w * 64;
-        char* st_dv = sdO;  // [sdO, sdS]
-        char* st_dk = sQ0;
-        {
-            unsigned v[64];
-            TM_LD32(tmem + lane_base + T_DV + c0, v);
-            TM_LD32(tmem + lane_base + T_DV + c0 + 32, (v + 32));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            stage_f32(st_dv, r, c0, v);
-            TM_LD32(tmem + lane_base + T_DK + c0, v);
-            TM_LD32(tmem + lane_base + T_DK + c0 + 32, (v + 32));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            stage_f32(st_dk, r, c0, v);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bar_ew();
-        if (warp == 4 && lane == 0) {
-            const int krow0 = it.seq_start + j * BKV;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                tma_reduce_add(&map_dv, st_dv + k * (kTile / 2), kvh * HD + 32 * k, krow0);
-                tma_reduce_add(&map_dk, st_dk + k * (kTile / 2), kvh * HD + 32 * k, krow0);
-            }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        if (lead && w == 1) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 1) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-    // no CTA of the pair leaves while the other may still arrive on its barriers
-    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
 // D[h][t] = sum_c dO[t][h][c] * O[t][h][c]; one warp per (t, h) row; also zeroes dq_acc rows
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ D, float* __restrict__ dq_acc, long long T, int H) {
@@ -1450,16 +994,10 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
         if (head_dim != HD) throw odcsim::ParamError("attn_bwd: head_dim must be 128");
         if (KV < 1 || H % KV) throw odcsim::ParamError("attn_bwd: H must be a multiple of KV");
         static thread_local int configured = -1;
-        static const bool use_t = [] {  // A/B while the transposed schedule is tuned
-            const char* e = std::getenv("ODC_ATTN_BWD");
-            return e && std::strcmp(e, "t") == 0;
-        }();
         int dev = 0;
         cudaGetDevice(&dev);
         if (configured != dev) {
             cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(attn_bwd_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwd4Smem);
             if (e != cudaSuccess) throw std::runtime_error(std::string("attn bwd smem attr: ") + cudaGetErrorString(e));
             configured = dev;
         }
@@ -1496,10 +1034,7 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
             a.dv_acc = dv_acc;
             a.T = T;
             odc::count_launch();
-            if (use_t)
-                attn_bwd_t_kernel<<<2 * n_items, kBwdThreads, kBwd4Smem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
-            else
-                attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
+            attn_bwd_kernel<<<n_items, kBwdThreads, kBwdSmem, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
         }
         *dq_out = dq_acc;
         *dk_out = dk_acc;
@@ -1507,12 +1042,6 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
     }
 }
 }  // namespace
-
-#ifdef ODC_ATTN_TRACE
-extern "C" int odc_attn_trace_read(unsigned long long* dst) {
-    return cudaMemcpyFromSymbol(dst, odc::attn::g_attn_trace, sizeof(odc::attn::g_attn_trace)) == cudaSuccess ? 0 : 1;
-}
-#endif
 
 extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
                                    const float* lse, void* dq, void* dk, void* dv, void* workspace,

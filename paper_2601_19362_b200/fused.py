@@ -3,8 +3,6 @@
 from __future__ import annotations
 
 import ctypes as C
-import os
-from typing import Optional
 
 import torch
 
@@ -109,24 +107,20 @@ def attn_fwd(q, k, v, items, scale):
     return out, lse
 
 
-def attn_bwd_items(lens, H: int, KV: int, device, sms: int = 148, pairs: Optional[bool] = None) -> torch.Tensor:
+def attn_bwd_items(lens, H: int, KV: int, device, sms: int = 148) -> torch.Tensor:
     """Backward work list: per (sequence, 128-key tile, kv head) the causal loop
     over (query head of the GQA group, query tile >= key tile). Loops longer
     than ~1/(2*SMs) of the total are cut into chunks (their dK/dV partials meet
-    in fp32 accumulators) so the grid load-balances; largest first (LPT).
-    pairs: items for the paired-CTA kernel (ODC_ATTN_BWD=t): one item per pair
-    of key tiles (2p, 2p+1), both walking query tiles >= 2p."""
-    if pairs is None:
-        pairs = os.environ.get("ODC_ATTN_BWD", "v2") == "t"
+    in fp32 accumulators) so the grid load-balances; largest first (LPT)."""
     G = H // KV
     loops, start = [], 0
     for n in lens:
         nt = (n + 127) // 128
-        for kt in range(0, nt, 2 if pairs else 1):
+        for kt in range(nt):
             loops.append((start, n, kt, G * (nt - kt)))
         start += n
     total = sum(t for *_, t in loops) * KV
-    chunk = max(32, -(-total // (sms if pairs else 2 * sms)))
+    chunk = max(32, -(-total // (2 * sms)))
     items = []
     for st, n, kt, t in loops:
         pieces = -(-t // chunk)

@@ -1,7 +1,8 @@
 """tcgen05 attention backward timing (CUDA events, 5 reps after a warm-up) on
 the verdict's shapes: one 32K sequence and 16 x 2K at H/KV 12/2, one 64K at
-40/8. One JSON line per case. A/B: ODC_ATTN_BWD=v2 (query-major scores) | t
-(transposed scores, P^T in TMEM; the default).
+40/8. One JSON line per case (A/B of kernel variants: build them with
+`python -m paper_2601_19362_b200.build --variant NAME DEFINE` and select with
+ODC_LIB_PATH; the label comes from ODC_ATTN_BWD).
 
 usage: python tools/attn_bwd_ab.py
 """
@@ -26,7 +27,7 @@ for lens, H, KV in (([32768], 12, 2), ([2048] * 16, 12, 2), ([8192, 6000, 4000, 
     bi = F.attn_bwd_items(lens, H, KV, "cuda")
     fl = sum(2 * 2 * s * s / 2 * 128 * H for s in lens) * 2.5  # 5 causal matmuls of the backward
     res = {"lens": lens[:3] + (["..."] if len(lens) > 3 else []), "n_seq": len(lens), "T": T, "H": H, "KV": KV,
-           "variant": os.environ.get("ODC_ATTN_BWD", "t")}
+           "variant": os.environ.get("ODC_ATTN_BWD", "shipped")}
     for name, fn in (("bwd", lambda: F.attn_bwd(q, k, v, o, do, lse, bi, sc)),
                      ("fwd", lambda: F.attn_fwd(q, k, v, F.attn_items(lens, H, "cuda"), sc))):
         fn()
