@@ -553,8 +553,8 @@ def run_sft(args):
                 "kernel": "odc::gemm::gemm2_kernel (tcgen05 cta_group::2, 256x256 tile per SM pair)",
                 "launches": gm["launches"], "ms_per_launch": round(gm["ms"] / gm["launches"], 4),
                 "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": ncu_traffic("gemm::gemm2_kernel")[0],
-                "traffic_source": f"{ncu_traffic('gemm::gemm2_kernel')[1]} (dram read+write per launch averaged over "
-                                  "the step's GEMM shapes, ncu --set full)"}
+                "traffic_source": f"{ncu_traffic('gemm::gemm2_kernel')[1]} (dram read+write per gemm2 launch, "
+                                  "averaged over the captured launches)"}
     pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
     # model FLOPs utilisation of the whole step: per sequence 6*P_nonembed*s (dense)
     # + 6*L*d*s^2 (causal attention, fwd+bwd) + 6*V*d*s (LM head); recompute is not counted
@@ -599,10 +599,12 @@ def run_sft(args):
 
 def ncu_traffic(kernel):
     """(dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`,
-    source file) from the newest committed ncu --set full capture summary
-    (profiles/r02/ncu_traffic.json, else r01)."""
-    for rnd in ("r02", "r01"):
-        path = os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")
+    source file) from the newest committed ncu capture summary: first the
+    capture of this bench's own launch mix (profiles/r02/ncu_traffic_bench.json:
+    every gemm2 launch of the first bench steps), else the per-shape capture
+    (profiles/r02/ncu_traffic.json), else round 1's."""
+    for name in ("r02/ncu_traffic_bench.json", "r02/ncu_traffic.json", "r01/ncu_traffic.json"):
+        path = os.path.join(ROOT, "profiles", name)
         try:
             with open(path) as f:
                 return json.load(f)["kernels"][kernel]["dram_bytes_per_launch"], os.path.relpath(path, ROOT)

@@ -18,6 +18,10 @@ S = bytes of one rank's bf16 parameter shard. Per rank and op:
                  the minibatch STORES w*g into this client's slot at every
                  owner (timed alone; the untimed minibatch_end between reps
                  releases the slots), fp32 wire bytes ((N-1)*2S)
+  conc_*         fetch (TMA) and push (RED or SLOT) of the same unit at the same
+                 time on two streams, as the backward overlaps them: each
+                 direction's GB/s over the pair's common time (fetch = rx,
+                 push = tx of this rank's NVLink ports)
   --sync         the paper's synchronous-launch protocol: every op
                  alone between barriers (torch barrier + device sync before
                  and after), time = max over ranks per op, averaged
@@ -146,14 +150,27 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         ops["odc_push_slot"] = ((lambda: sl.push(0, grad, 1.0)), (world - 1) * 2 * S, lambda: sl.minibatch_end())
+        side = torch.cuda.Stream(device=dev)
+
+        def concurrent(pusher):
+            side.wait_stream(stream)
+            eng.fetch(0, full, stream=stream)
+            pusher.push(0, grad, 1.0, stream=side)
+            stream.wait_stream(side)
+
+        for tag, pusher, after in (("red", eng, None), ("slot", sl, lambda: sl.minibatch_end())):
+            ops[f"conc_{tag}"] = ((lambda p=pusher: concurrent(p)), {"fetch": (world - 1) * S, "push": (world - 1) * 2 * S},
+                                  after)
         for name, op in ops.items():
             fn, nbytes = op[0], op[1]
             ms = timed(fn, reps, op[2] if len(op) > 2 else None)
-            row = {"op": name, "world": world, "shard_bytes": S, "ms": round(ms, 5),
-                   "GBps": round(nbytes / (ms / 1e3) / 1e9, 1)}
-            rows.append(row)
-            if rank == 0:
-                print(json.dumps(row), flush=True)
+            parts = nbytes.items() if isinstance(nbytes, dict) else [(None, nbytes)]
+            for part, nb in parts:
+                row = {"op": name if part is None else f"{name}:{part}", "world": world, "shard_bytes": S,
+                       "ms": round(ms, 5), "GBps": round(nb / (ms / 1e3) / 1e9, 1)}
+                rows.append(row)
+                if rank == 0:
+                    print(json.dumps(row), flush=True)
         for e2 in [eng] + extra:
             e2.minibatch_end()
         for e2 in [eng] + extra:
@@ -164,7 +181,8 @@ def main():
     if rank == 0:
         os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
         sizes = sorted({r["shard_bytes"] for r in rows})
-        names = ["odc_fetch", "odc_fetch_ce", "nccl_all_gather", "odc_push", "odc_push_slot", "nccl_reduce_scatter"]
+        names = ["odc_fetch", "odc_fetch_ce", "nccl_all_gather", "odc_push", "odc_push_slot", "nccl_reduce_scatter",
+                 "conc_red:fetch", "conc_red:push", "conc_slot:fetch", "conc_slot:push"]
         names += sorted({r["op"] for r in rows} - set(names))
         with open(args.out, "w") as f:
             f.write(f"# P2P fetch/push vs NCCL, N={world} (GB/s of algorithmic NVLink bytes per rank)"
