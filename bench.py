@@ -497,7 +497,12 @@ def run_sft(args):
         with ctx:  # nvidia-smi clock/throttle sampling covers exactly the timed steps
             a.record(stream)
             for k in timed_steps:
+                nvtx = os.environ.get("ODC_NVTX_STEP") and k == timed_steps[0]  # ncu --nvtx-include odc_step/
+                if nvtx:
+                    torch.cuda.nvtx.range_push("odc_step")
                 t0, t1, t2, loss = one(k, pre.get(k))
+                if nvtx:
+                    torch.cuda.nvtx.range_pop()
                 evs.append((t0, t1, t2))
                 if not resident:
                     losses.append(loss.item())  # D2H of the step's result (e2e)
@@ -505,7 +510,8 @@ def run_sft(args):
             torch.cuda.synchronize()
         launches = _lib.kernel_launches() - n0
         chk()
-        log(comm.name, "timed steps done", a.elapsed_time(z), "ms")
+        log(comm.name, "timed steps done", a.elapsed_time(z), "ms; per step",
+            [round(e0.elapsed_time(e2), 2) for e0, _, e2 in evs])
         gsum = G.recorder.summary() if record else None
         G.recorder = None
         ms = a.elapsed_time(z)
@@ -555,6 +561,10 @@ def run_sft(args):
                 "gemm_share_of_step": round(gm["ms"] / res["ms"], 4), "traffic": ncu_traffic("gemm::gemm2_kernel")[0],
                 "traffic_source": f"{ncu_traffic('gemm::gemm2_kernel')[1]} (dram read+write per gemm2 launch, "
                                   "averaged over the captured launches)"}
+        if gm.get("alg_bytes"):
+            roof["algorithmic_bytes_per_launch"] = int(gm["alg_bytes"] / gm["launches"])
+            if roof["traffic"]:
+                roof["traffic_over_algorithmic"] = round(roof["traffic"] / roof["algorithmic_bytes_per_launch"], 3)
     pred = analytic(lens, plan_odc, plan_fsdp, beta, timed_steps)
     # model FLOPs utilisation of the whole step: per sequence 6*P_nonembed*s (dense)
     # + 6*L*d*s^2 (causal attention, fwd+bwd) + 6*V*d*s (LM head); recompute is not counted

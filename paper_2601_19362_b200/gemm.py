@@ -26,12 +26,23 @@ class Recorder:
     def __init__(self):
         self.rows = []
 
+    @staticmethod
+    def alg_bytes(key):
+        """Operand + result bytes of one launch: bf16 A [M,K] and B [N,K], the output (fp32 or bf16, read
+        too when accumulating), the fused residual; the SwiGLU launch writes gu [T,2F] and m [T,F]."""
+        M, N, K, _, _, f32, acc, res = key
+        if res == "glu":
+            return 2 * (M * K + N * K) + 2 * M * N + 2 * M * (N // 2)
+        out = (4 if f32 else 2) * M * N
+        return 2 * (M * K + N * K) + out * (2 if acc else 1) + (2 * M * N if res else 0)
+
     def summary(self):
         if not self.rows:
             return None
         ms = [r[1].elapsed_time(r[2]) for r in self.rows]
         fl = sum(r[0] for r in self.rows)
-        return {"launches": len(self.rows), "flops": fl, "ms": sum(ms)}
+        return {"launches": len(self.rows), "flops": fl, "ms": sum(ms),
+                "alg_bytes": sum(self.alg_bytes(r[3]) for r in self.rows)}
 
 
 recorder = None
