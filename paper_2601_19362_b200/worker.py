@@ -27,7 +27,9 @@ Comm backends share one interface:
 """
 from __future__ import annotations
 
+import contextlib
 import math
+import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -97,6 +99,23 @@ def rope_tables(positions: torch.Tensor, head_dim: int):
     inv = 1.0 / (ROPE_THETA ** (torch.arange(0, head_dim, 2, device=positions.device, dtype=torch.float32) / head_dim))
     ang = positions.float()[:, None] * inv[None, :]
     return torch.cos(ang), torch.sin(ang)  # [T, hd/2]
+
+
+# NVTX ranges per fetch / layer forward / LM head / layer backward / push / barrier+AdamW,
+# for ncu/nsys (`ncu --nvtx --nvtx-include "bwd l3/"`); off unless ODC_NVTX=1
+_NVTX = os.environ.get("ODC_NVTX") == "1"
+
+
+@contextlib.contextmanager
+def nvtx(name: str):
+    if not _NVTX:
+        yield
+        return
+    torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        torch.cuda.nvtx.range_pop()
 
 
 # ------------------------------------------------------------------ comm
@@ -345,7 +364,8 @@ class Worker:
         if after is not None:
             self.comm_stream.wait_event(after)
         tr = self.tracer.span("gather", unit, self.comm_stream, True, buf.numel()) if self.tracer else None
-        self.comm.fetch(unit, buf, self.comm_stream)
+        with nvtx(f"fetch u{unit}"):
+            self.comm.fetch(unit, buf, self.comm_stream)
         if tr:
             Tracer.end(tr, self.comm_stream)
         ev = torch.cuda.Event()
@@ -417,7 +437,8 @@ class Worker:
             if l < L:  # prefetch the next unit into the other buffer once layer l-1 released it
                 ev = self._fetch_unit(l + 1, after=_record(cur))
             tr = self.tracer.span("fwd", l, cur, False) if self.tracer else None
-            act, h = self._layer_fwd(P, h, b)
+            with nvtx(f"fwd l{l}"):
+                act, h = self._layer_fwd(P, h, b)
             saved.append(self._keep(act))
             if tr:
                 Tracer.end(tr, cur)
@@ -433,10 +454,11 @@ class Worker:
         loss = torch.zeros((), device=self.dev, dtype=torch.float32)
         for c0 in range(0, T, self.ce_chunk):
             c1 = min(T, c0 + self.ce_chunk)
-            logits = G.linear_fwd(hf[c0:c1], head)
-            dl = F.ce_fwd_bwd_(logits, b.labels[c0:c1], 1.0 / n_valid, loss)  # logits -> dlogits in place
-            G.linear_dgrad(dl, head, out=dhf[c0:c1])
-            G.linear_wgrad(dl, hf[c0:c1], out=headg, accumulate=True)
+            with nvtx(f"lm_head+ce {c0}"):
+                logits = G.linear_fwd(hf[c0:c1], head)
+                dl = F.ce_fwd_bwd_(logits, b.labels[c0:c1], 1.0 / n_valid, loss)  # logits -> dlogits in place
+                G.linear_dgrad(dl, head, out=dhf[c0:c1])
+                G.linear_wgrad(dl, hf[c0:c1], out=headg, accumulate=True)
             del logits, dl
         loss /= n_valid
         dh = F.rmsnorm_bwd(dhf, h, E["norm"], rf, EG["norm"])
@@ -462,6 +484,8 @@ class Worker:
                 if name in Gv:
                     Gv[name].zero_()
             tr = self.tracer.span("bwd", l, cur, False) if self.tracer else None
+            rng = nvtx(f"bwd l{l}")
+            rng.__enter__()
             x, a, r1, q, k, v, o, lse, hm, bn, r2, gu, m = self._restore(P, saved[l - 1], b)
             # MLP block
             dm = G.linear_dgrad(dh, P["down_w"])
@@ -483,12 +507,14 @@ class Worker:
             da = G.linear_dgrad(dqkv, P["qkv_w"])
             G.linear_wgrad(dqkv, a, out=Gv["qkv_w"])
             dh = F.rmsnorm_bwd(da, x, P["ln1"], r1, Gv["ln1"], resid=dhm)
+            rng.__exit__(None, None, None)
             if tr:
                 Tracer.end(tr, cur)
             # push this unit's gradient as soon as it is complete
             self.comm_stream.wait_event(_record(cur))
             trp = self.tracer.span("reduce", l, self.comm_stream, True, self.gbuf[gi].numel()) if self.tracer else None
-            self.comm.push(l, self.gbuf[gi], weight, self.comm_stream)
+            with nvtx(f"push u{l}"):
+                self.comm.push(l, self.gbuf[gi], weight, self.comm_stream)
             if trp:
                 Tracer.end(trp, self.comm_stream)
             push_ev[gi] = _record(self.comm_stream)
@@ -527,8 +553,9 @@ class Worker:
             self.cache_ev = [None] * (self.L + 1)
         cur = torch.cuda.current_stream(self.dev)
         self.comm_stream.wait_event(_record(cur))
-        self.comm.minibatch_end(self.comm_stream)
-        self.comm.adam(self.comm_stream, lr=lr)
+        with nvtx("barrier+adamw"):
+            self.comm.minibatch_end(self.comm_stream)
+            self.comm.adam(self.comm_stream, lr=lr)
         cur.wait_event(_record(self.comm_stream))
 
 

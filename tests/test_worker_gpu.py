@@ -200,3 +200,25 @@ def test_trace_schema_and_idle_fraction():
     assert idle == pytest.approx(O.bubble_rate(busy, total), abs=1e-12)
     assert 0.0 <= idle < 1.0
     eng.check()
+
+
+def test_nvtx_ranges_do_not_change_the_step(monkeypatch):
+    """NVTX ranges around fetch / layer fwd / LM head / layer bwd /
+    push / barrier+AdamW (ODC_NVTX=1) only annotate; the step is unchanged."""
+    s = TINY
+    sizes = W.unit_sizes(s)
+    gen = torch.Generator(device=DEV).manual_seed(6)
+    units = [W.init_unit(s, u, gen, DEV) for u in range(len(sizes))]
+    lens = [37, 100, 63, 200]
+    losses = []
+    for on in (False, True):
+        monkeypatch.setattr(W, "_NVTX", on)
+        eng = OdcEngine(sizes, push_mode="slot")
+        for u, t in enumerate(units):
+            eng.set_params(u, t)
+        wk = W.Worker(s, W.OdcComm(eng), DEV, ce_chunk=128)
+        losses.append(wk.microbatch(W.make_batch(lens, [0, 1, 2, 3], s.vocab, DEV), 1.0).item())
+        wk.minibatch_end()
+        eng.check()
+        eng.close()
+    assert losses[0] == pytest.approx(losses[1], rel=1e-5)
