@@ -1,0 +1,11 @@
+# round 2, call ac: attention backward (split P/dS store) with 1 exp2 pair in 2 / in 4 / none on the FMA pipe
+set -x
+D=gpurun_out/r02ac
+mkdir -p $D
+timeout -s KILL 300 python -m pytest tests/test_attention_gpu.py -q -x --timeout 240 -p no:cacheprovider > $D/tests.log 2>&1
+tail -n 2 $D/tests.log
+for v in poly2 poly0 poly4 poly2 poly0 poly4; do
+  if [ $v = poly2 ]; then L=paper_2601_19362_b200/lib/libodc.so; else L=paper_2601_19362_b200/lib/variants/$v/libodc.so; fi
+  ODC_LIB_PATH=$L ODC_ATTN_BWD=$v timeout -s KILL 300 python tools/attn_bwd_ab.py >> $D/attn_ab.jsonl 2>&1
+done
+grep -o '"T": [0-9]*, "H": [0-9]*.*"variant": "[a-z0-9]*", "bwd_ms": [0-9.]*, "bwd_tflops": [0-9.]*' $D/attn_ab.jsonl
