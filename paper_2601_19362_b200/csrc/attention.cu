@@ -539,8 +539,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // sdp_full: S_n and dP_n in TMEM; ds_full: P_n / dS_n in smem (S_n, dP_n consumed);
     // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
     // s_read: S_n, dP_n are in the elementwise warps' registers (S columns free for S_{n+1})
+    // p_full: P_n in smem (dV_n may start; the dS store may still wait for the dQ staging drain)
     __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, s_read,
-        ds_full, dq_full, dq_read;
+        p_full, ds_full, dq_full, dq_read;
     __shared__ unsigned tmem_base;
 
     const BwdItem it = g.items[blockIdx.x];
@@ -571,6 +572,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                    su32(&do_full), su32(&do_empty), su32(&sdp_full), su32(&s_read), su32(&ds_full), su32(&dq_full),
                    su32(&dq_read), it.it_end - it.it_begin);
 #endif
+        mbar_init(&p_full, 8);
         mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
         mbar_init(&dq_read, 8);
@@ -643,13 +645,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mbar_wait(&s_read, n & 1);
                     issue_s(n + 1);
                 }
-                mbar_wait(&ds_full, n & 1);  // P, dS in smem
+                mbar_wait(&p_full, n & 1);  // P in smem (dS may still be waiting for the staging drain)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk)  // K = query rows: MN-major A (P^T) and B (dO)
                     mma(tmem + T_DV, sdesc(pa + kk * 2048, kTile / 2, 1024), sdesc(doa + kk * 2048, kTile / 2, 1024),
                         id_mm, (n > 0 || kk > 0));
                 commit(&do_empty);  // dO_n consumed: the TMA refills it while dK, dQ run
+                mbar_wait(&ds_full, n & 1);  // dS in smem
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
                     mma(tmem + T_DK, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024),
@@ -707,37 +711,53 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #ifdef ODC_ATTN_DEBUG
             if (lane == 0 && blockIdx.x == 0) printf("ew warp %d n %d s_read\n", warp, n);
 #endif
-            // P = exp2(S*scale*log2e - lse2) (0 where masked), dS = P * (dP*scale - D*scale), packed bf16 in
-            // place; packed fp32x2 math, and no mask work on tiles this row sees entirely
+            // P = exp2(S*scale*log2e - lse2) (0 where masked), dS = P * (dP*scale - D*scale); packed fp32x2
+            // math, no mask work on tiles this row sees entirely. P first (kept in fp32 in sv, packed to pk),
+            // stored and signalled so dV_n runs on the tensor pipe while dS is computed and stored.
             const float2 v_sl2 = make_float2(sl2, sl2), v_nlse = make_float2(-lse2, -lse2);
             const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
+            unsigned pk[32];
             if (lim >= 63) {
 #pragma unroll
                 for (int x = 0; x < 64; x += 2) {
                     const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
                     const float2 pp = make_float2(ex2(t.x), ex2(t.y));
-                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
-                    const float2 d = fmul2(pp, u);
-                    sv[x / 2] = pack_bf16(pp.x, pp.y);
-                    dp[x / 2] = pack_bf16(d.x, d.y);
+                    sv[x] = __float_as_uint(pp.x);
+                    sv[x + 1] = __float_as_uint(pp.y);
+                    pk[x / 2] = pack_bf16(pp.x, pp.y);
                 }
             } else {
 #pragma unroll
                 for (int x = 0; x < 64; x += 2) {
                     const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
                     const float2 pp = make_float2(x > lim ? 0.f : ex2(t.x), x + 1 > lim ? 0.f : ex2(t.y));
-                    const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
-                    const float2 d = fmul2(pp, u);
-                    sv[x / 2] = pack_bf16(pp.x, pp.y);
-                    dp[x / 2] = pack_bf16(d.x, d.y);
+                    sv[x] = __float_as_uint(pp.x);
+                    sv[x + 1] = __float_as_uint(pp.y);
+                    pk[x / 2] = pack_bf16(pp.x, pp.y);
                 }
             }
-            if (n > 0) {  // the staging of dQ_{n-1} (= sP / sdS) has been read by its TMA reduction
+            // dQ_{n-1} was staged as two bulk groups, sP's half first: P waits for that half's read
+            // only, and dV_n starts on P while the sdS half still drains into L2
+            if (n > 0) {
+                if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                bar_ew();
+            }
+            store_swizzled(sP, r, c0, pk);
+            store_swizzled(sP, r, c0 + 32, pk + 16);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full);
+#pragma unroll
+            for (int x = 0; x < 64; x += 2) {
+                const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
+                const float2 d = fmul2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), u);
+                dp[x / 2] = pack_bf16(d.x, d.y);
+            }
+            if (n > 0) {
                 if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 bar_ew();
             }
-            store_swizzled(sP, r, c0, sv);
-            store_swizzled(sP, r, c0 + 32, sv + 16);
             store_swizzled(sdS, r, c0, dp);
             store_swizzled(sdS, r, c0 + 32, dp + 16);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -763,8 +783,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
+                    if (k & 1) asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // sP half, sdS half
                 }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
         // dK, dV of the key tile (complete: the last dq_full covers every MMA) -> staging -> TMA reduce-add
