@@ -540,8 +540,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // dq_full: every MMA of n done (dQ_n in the dP columns); dq_read: dQ_n read out
     // s_read: S_n, dP_n are in the elementwise warps' registers (S columns free for S_{n+1})
     // p_full: P_n in smem (dV_n may start; the dS store may still wait for the dQ staging drain)
+    // dk_done: dK_n finished reading dS_n (warpgroup 1 may stage its dQ half into sdS)
     __shared__ __align__(8) unsigned long long kv_full, q_full[2], q_empty[2], do_full, do_empty, sdp_full, s_read,
-        p_full, ds_full, dq_full, dq_read;
+        p_full, ds_full, dq_full, dq_read, dk_done;
     __shared__ unsigned tmem_base;
 
     const BwdItem it = g.items[blockIdx.x];
@@ -573,6 +574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                    su32(&dq_read), it.it_end - it.it_begin);
 #endif
         mbar_init(&p_full, 8);
+        mbar_init(&dk_done, 1);
         mbar_init(&ds_full, 8);
         mbar_init(&dq_full, 1);
         mbar_init(&dq_read, 8);
@@ -654,17 +656,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 commit(&do_empty);  // dO_n consumed: the TMA refills it while dK, dQ run
                 mbar_wait(&ds_full, n & 1);  // dS in smem
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-                for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
-                    mma(tmem + T_DK, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024),
-                        id_mm, (n > 0 || kk > 0));
-                commit(&q_empty[b]);
+                // dQ first: its read-out (and dP_{n+1}'s wait for it) overlaps dK
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
                     const unsigned aoff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
                     mma(tmem + T_DP, sdesc(dsa + aoff, 16, 1024), sdesc(ka + kk * 2048, kTile / 2, 1024), id_km, kk > 0);
                 }
-                commit(&dq_full);  // also: P, dS consumed
+                commit(&dq_full);  // also: P consumed (dV was issued before)
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
+                    mma(tmem + T_DK, sdesc(dsa + kk * 2048, kTile / 2, 1024), sdesc(qa + kk * 2048, kTile / 2, 1024),
+                        id_mm, (n > 0 || kk > 0));
+                commit(&q_empty[b]);
+                commit(&dk_done);  // dS consumed
             }
         }
       }
@@ -675,7 +679,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #endif
         const int quad = warp % 4;
         const int c0 = ((warp - 4) >> 2) * 64;  // this warp's 64 columns
-        const bool lead = warp == 4 && lane == 0;  // issues the TMA reductions
+        const int wg = (warp - 4) >> 2;
+        const bool lead = (warp & 3) == 0 && lane == 0;  // per warpgroup: issues its half's TMA reductions
         const int r = quad * 32 + lane;  // row: query within tile i (loop) / key within tile j (epilogue)
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
         const float sl2 = g.scale_log2, sc = g.scale;
@@ -736,10 +741,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     pk[x / 2] = pack_bf16(pp.x, pp.y);
                 }
             }
-            // dQ_{n-1} was staged as two bulk groups, sP's half first: P waits for that half's read
-            // only, and dV_n starts on P while the sdS half still drains into L2
+            // dQ_{n-1} was staged per warpgroup: warpgroup 0's half in sP, warpgroup 1's in sdS (each
+            // lead committed its own bulk group). P waits for the sP half's read only, and dV_n runs
+            // on P while the sdS half still drains into L2
             if (n > 0) {
-                if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                if (lead && wg == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 bar_ew();
             }
             store_swizzled(sP, r, c0, pk);
@@ -755,7 +761,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 dp[x / 2] = pack_bf16(d.x, d.y);
             }
             if (n > 0) {
-                if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (lead && wg == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 bar_ew();
             }
             store_swizzled(sdS, r, c0, dp);
@@ -775,19 +781,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&dq_read);
+            // warpgroup 0's half goes to sP (free: dV_n read P before dQ_n), warpgroup 1's to sdS once
+            // dK_n has read dS
+            if (wg == 1) mbar_wait(&dk_done, n & 1);
             stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bar_ew();
+            asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
             if (lead) {
                 const int row0 = it.seq_start + i * BQ;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    tma_reduce_add(&map_dq, stage + k * (kTile / 2), h * HD + 32 * k, row0);
-                    if (k & 1) asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // sP half, sdS half
-                }
+                for (int k = 0; k < 2; ++k)
+                    tma_reduce_add(&map_dq, stage + (2 * wg + k) * (kTile / 2), h * HD + c0 + 32 * k, row0);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
-        // dK, dV of the key tile (complete: the last dq_full covers every MMA) -> staging -> TMA reduce-add
+        // dK, dV of the key tile (every MMA done once the last dK finished) -> staging -> TMA reduce-add
+        if (n_iter > 0) mbar_wait(&dk_done, (n_iter - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         bar_ew();
@@ -806,7 +815,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_ew();
-        if (lead) {
+        if (lead && wg == 0) {
             const int krow0 = it.seq_start + j * BKV;  // key rows past the sequence end hold exact zeros
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -814,8 +823,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 tma_reduce_add(&map_dk, st_dk + k * (kTile / 2), kvh * HD + 32 * k, krow0);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
+        if (lead) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
