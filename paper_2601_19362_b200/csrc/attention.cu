@@ -199,6 +199,20 @@ __device__ __forceinline__ void commit(unsigned long long* bar) {
         "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                                     \
         : "memory")
 
+#ifdef ODC_ATTN_TRACE
+// per-iteration SM clock stamps of the backward's CTA 0 (tools/attn_bwd_trace.py): [event][iteration]
+constexpr int kTrEvents = 21, kTrIters = 64;
+__device__ unsigned long long g_attn_trace[kTrEvents * kTrIters];
+#define TR(ev, n)                                                                                  \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && (n) < kTrIters) g_attn_trace[(ev) * kTrIters + (n)] = clock64();    \
+    } while (0)
+#else
+#define TR(ev, n) \
+    do {          \
+    } while (0)
+#endif
+
 struct Item {
     int seq_start, seq_len, q_tile, head;
 };
@@ -637,6 +651,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 if (n > 0) mbar_wait(&dq_read, (n - 1) & 1);  // dP columns free again
                 mbar_wait(&do_full, n & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TR(0, n);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {  // dP = dO V^T
                     const unsigned off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
@@ -645,10 +660,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 commit(&sdp_full);
                 if (n + 1 < n_iter) {  // S_{n+1} overlaps the elementwise work of n once S_n is in registers
                     mbar_wait(&s_read, n & 1);
+                    TR(1, n);
                     issue_s(n + 1);
                 }
                 mbar_wait(&p_full, n & 1);  // P in smem (dS may still be waiting for the staging drain)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TR(2, n);
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk)  // K = query rows: MN-major A (P^T) and B (dO)
                     mma(tmem + T_DV, sdesc(pa + kk * 2048, kTile / 2, 1024), sdesc(doa + kk * 2048, kTile / 2, 1024),
@@ -656,6 +673,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 commit(&do_empty);  // dO_n consumed: the TMA refills it while dK, dQ run
                 mbar_wait(&ds_full, n & 1);  // dS in smem
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TR(3, n);
                 // dQ first: its read-out (and dP_{n+1}'s wait for it) overlaps dK
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {  // dQ = dS K into the dP columns
@@ -669,6 +687,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         id_mm, (n > 0 || kk > 0));
                 commit(&q_empty[b]);
                 commit(&dk_done);  // dS consumed
+                TR(4, n);
             }
         }
       }
@@ -704,6 +723,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV - c0 : -1;  // visible keys among our columns
             mbar_wait(&sdp_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lead) TR(5 + 8 * wg, n);
             unsigned sv[64], dp[64];
             TM_LD32(tmem + lane_base + T_S + c0, sv);
             TM_LD32(tmem + lane_base + T_S + c0 + 32, (sv + 32));
@@ -745,7 +765,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // lead committed its own bulk group). P waits for the sP half's read only, and dV_n runs
             // on P while the sdS half still drains into L2
             if (n > 0) {
-                if (lead && wg == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (lead && wg == 0) {
+                    TR(6, n);
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    TR(7, n);
+                }
                 bar_ew();
             }
             store_swizzled(sP, r, c0, pk);
@@ -754,6 +778,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full);
+            if (lead) TR(8 + 6 * wg, n);
 #pragma unroll
             for (int x = 0; x < 64; x += 2) {
                 const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
@@ -761,7 +786,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 dp[x / 2] = pack_bf16(d.x, d.y);
             }
             if (n > 0) {
-                if (lead && wg == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (lead && wg == 1) {
+                    TR(15, n);
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    TR(16, n);
+                }
                 bar_ew();
             }
             store_swizzled(sdS, r, c0, dp);
@@ -770,10 +799,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&ds_full);
+            if (lead) TR(9 + 8 * wg, n);
             // dQ_n (fp32, already scaled) -> smem staging -> TMA reduce-add into the global accumulator,
             // while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lead) TR(10 + 8 * wg, n);
             unsigned v[64];
             TM_LD32(tmem + lane_base + T_DP + c0, v);
             TM_LD32(tmem + lane_base + T_DP + c0 + 32, (v + 32));
@@ -784,6 +815,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // warpgroup 0's half goes to sP (free: dV_n read P before dQ_n), warpgroup 1's to sdS once
             // dK_n has read dS
             if (wg == 1) mbar_wait(&dk_done, n & 1);
+            if (lead) TR(11 + 8 * wg, n);
             stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
@@ -793,6 +825,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int k = 0; k < 2; ++k)
                     tma_reduce_add(&map_dq, stage + (2 * wg + k) * (kTile / 2), h * HD + c0 + 32 * k, row0);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                TR(12 + 8 * wg, n);
             }
         }
         // dK, dV of the key tile (every MMA done once the last dK finished) -> staging -> TMA reduce-add
@@ -1071,6 +1104,12 @@ void attn_bwd_accumulate(const void* q, const void* k, const void* v, const void
     }
 }
 }  // namespace
+
+#ifdef ODC_ATTN_TRACE
+extern "C" int odc_attn_trace_read(unsigned long long* dst) {
+    return cudaMemcpyFromSymbol(dst, odc::attn::g_attn_trace, sizeof(odc::attn::g_attn_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" odc_status odc_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
                                    const float* lse, void* dq, void* dk, void* dv, void* workspace,
