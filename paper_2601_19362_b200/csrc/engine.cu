@@ -71,6 +71,24 @@ void cuda_ok(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Makes `d` the current device for one API call and restores the caller's device on return, so a
+// call on one rank's context never leaves another device current behind the caller (e.g. torch).
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int d) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        if (prev_ != d) cuda_ok(cudaSetDevice(d), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        if (prev_ >= 0) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+  private:
+    int prev_ = -1;
+};
+
 constexpr std::int64_t kFlagsBytes = 4096;
 constexpr std::int64_t kDoneOff = 0;
 constexpr std::int64_t kEpochOff = 1024;
@@ -165,7 +183,7 @@ struct odc_ctx {
     void need_ready() const {
         if (!ready) throw StateError("odc context used before odc_ctx_ready()");
     }
-    void dev() const { cuda_ok(cudaSetDevice(cfg.device), "cudaSetDevice"); }
+    int dev_id() const { return cfg.device; }
     bool red_mode() const { return cfg.push_mode == ODC_PUSH_RED; }
     // RED: the caller is done with last minibatch's grad shards (this is the
     // next ODC call after odc_minibatch_end without an AdamW step): zero them
@@ -316,7 +334,7 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
             }
             c->arena_bytes = off;
             c->layout_hash = h;
-            c->dev();
+            DeviceGuard dg(c->dev_id());
             cuda_ok(odc::preload_kernels(), "preload kernels");
             cuda_ok(cudaMalloc(&c->arena, static_cast<std::size_t>(off)), "cudaMalloc arena");
             cuda_ok(cudaMemset(c->arena, 0, static_cast<std::size_t>(off)), "memset arena");
@@ -340,7 +358,7 @@ odc_status odc_ctx_create(const odc_config* cfg, odc_ctx_t* out) {
 
 odc_status odc_ctx_destroy(odc_ctx_t c) {
     if (!c) return ODC_OK;
-    cudaSetDevice(c->cfg.device);
+    DeviceGuard dg(c->cfg.device);
     cudaDeviceSynchronize();
     for (int r = 0; r < static_cast<int>(c->peer.size()); ++r)
         if (r != c->cfg.rank && c->peer[static_cast<std::size_t>(r)] &&
@@ -360,7 +378,7 @@ odc_status odc_ctx_export(odc_ctx_t ch, void* blob, std::size_t cap, std::size_t
         odc_ctx* c = C(ch);
         if (len) *len = sizeof(Blob);
         if (!blob || cap < sizeof(Blob)) throw ParamError("export buffer too small");
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         Blob b{};
         b.magic = kBlobMagic;
         b.rank = c->rank();
@@ -384,7 +402,7 @@ odc_status odc_ctx_import(odc_ctx_t ch, int peer, const void* blob, std::size_t 
             throw ParamError("IPC blob does not belong to this peer/world");
         if (b.layout_hash != c->layout_hash || b.arena_bytes != c->arena_bytes)
             throw ParamError("peer arena layout differs (different layer sizes or push mode)");
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         void* p = nullptr;
         cuda_ok(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
         c->peer[static_cast<std::size_t>(peer)] = static_cast<char*>(p);
@@ -401,7 +419,7 @@ odc_status odc_ctx_import_ctx(odc_ctx_t ch, int peer, odc_ctx_t peer_ctx) {
         if (p->rank() != peer || p->world() != c->world()) throw ParamError("context does not belong to this peer/world");
         if (p->layout_hash != c->layout_hash || p->arena_bytes != c->arena_bytes)
             throw ParamError("peer arena layout differs (different layer sizes or push mode)");
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         if (p->cfg.device != c->cfg.device) {  // another GPU of this process: direct peer access over NVLink
             int ok = 0;
             cuda_ok(cudaDeviceCanAccessPeer(&ok, c->cfg.device, p->cfg.device), "cudaDeviceCanAccessPeer");
@@ -421,7 +439,7 @@ odc_status odc_ctx_ready(odc_ctx_t ch) {
         odc_ctx* c = C(ch);
         for (int r = 0; r < c->world(); ++r)
             if (!c->imported[static_cast<std::size_t>(r)]) throw StateError("peer " + std::to_string(r) + " not imported");
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         // AdamW segment table over this rank's owned shards
         std::vector<odc::AdamSeg> segs;
         std::vector<std::int64_t> start{0};
@@ -458,7 +476,7 @@ odc_status odc_set_params(odc_ctx_t ch, int layer, const float* src_full, void* 
         odc_ctx* c = C(ch);
         c->need_ready();
         const Unit& u = c->unit(layer);
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         const int r = c->rank();
         c->drain_pending(S(stream));
         cuda_ok(odc::launch_init_shard(c->f32_of(r, u.off_master, u), c->param_of(r, u), src_full + u.begin(r), u.len(r),
@@ -472,7 +490,7 @@ odc_status odc_fetch(odc_ctx_t ch, int layer, void* dst_full, void* stream) {
         odc_ctx* c = C(ch);
         c->need_ready();
         const Unit& u = c->unit(layer);
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         c->drain_pending(S(stream));
         odc::SegTable t{};
         t.n = c->world();
@@ -495,7 +513,7 @@ odc_status odc_fetch_master(odc_ctx_t ch, int layer, float* dst_full, void* stre
         odc_ctx* c = C(ch);
         c->need_ready();
         const Unit& u = c->unit(layer);
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         odc::SegTable t{};
         t.n = c->world();
         for (int i = 0; i < c->world(); ++i) {
@@ -519,7 +537,7 @@ odc_status odc_push(odc_ctx_t ch, int layer, const void* grad_full, int grad_dty
         const Unit& u = c->unit(layer);
         if (grad_dtype != ODC_F32 && grad_dtype != ODC_BF16) throw ParamError("grad dtype must be ODC_F32 or ODC_BF16");
         const bool bf16 = grad_dtype == ODC_BF16;
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         c->drain_pending(S(stream));
         if (c->slot_mode()) {
             // w*g for every owner goes straight into this client's slot AT THE OWNER over NVLink:
@@ -618,7 +636,7 @@ odc_status odc_push_slice(odc_ctx_t ch, int layer, int target, std::int64_t offs
                                 std::to_string(u.block));
         if (offset < 0 || offset + n > u.len(target)) throw ProtocolError("payload does not fit the target shard");
         if (n == 0) return;
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         c->drain_pending(S(stream));
         if (c->slot_mode()) {
             const int me = c->rank();
@@ -672,7 +690,7 @@ odc_status odc_minibatch_end(odc_ctx_t ch, void* stream) {
     return odc::guard([&] {
         odc_ctx* c = C(ch);
         c->need_ready();
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         c->drain_pending(S(stream));
         odc::BarrierArgs a{};
         a.world = c->world();
@@ -732,7 +750,7 @@ odc_status odc_read_grad_shard(odc_ctx_t ch, int layer, float* dst, void* stream
         odc_ctx* c = C(ch);
         c->need_ready();
         const Unit& u = c->unit(layer);
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         const int r = c->rank();
         if (u.len(r) > 0)
             cuda_ok(cudaMemcpyAsync(dst, c->f32_of(r, u.off_grad, u), static_cast<std::size_t>(u.len(r)) * 4,
@@ -746,7 +764,7 @@ odc_status odc_read_master_shard(odc_ctx_t ch, int layer, float* dst, void* stre
         odc_ctx* c = C(ch);
         c->need_ready();
         const Unit& u = c->unit(layer);
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         const int r = c->rank();
         if (u.len(r) > 0)
             cuda_ok(cudaMemcpyAsync(dst, c->f32_of(r, u.off_master, u), static_cast<std::size_t>(u.len(r)) * 4,
@@ -760,7 +778,7 @@ odc_status odc_adam_step(odc_ctx_t ch, const odc_adam_cfg* cfg, void* stream) {
         odc_ctx* c = C(ch);
         c->need_ready();
         if (!cfg || cfg->step < 1) throw ParamError("adam step must be >= 1");
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         odc::AdamArgs a{};
         a.segs = c->d_segs;
         a.nseg = static_cast<int>(c->units.size());
@@ -787,7 +805,7 @@ odc_status odc_ctx_check(odc_ctx_t ch, void* stream) {
     unsigned long long e = 0;
     odc_status st = odc::guard([&] {
         odc_ctx* c = C(ch);
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         cuda_ok(cudaStreamSynchronize(S(stream)), "sync");
         cuda_ok(cudaMemcpy(&e, c->err(), 8, cudaMemcpyDeviceToHost), "read err");
     });
@@ -809,7 +827,7 @@ odc_status odc_ctx_flags(odc_ctx_t ch, uint64_t* flags, void* stream) {
     return odc::guard([&] {
         odc_ctx* c = C(ch);
         if (!flags) throw ParamError("null flags");
-        c->dev();
+        DeviceGuard dg(c->dev_id());
         cuda_ok(cudaStreamSynchronize(S(stream)), "sync");
         unsigned long long e = 0;
         cuda_ok(cudaMemcpy(&e, c->err(), 8, cudaMemcpyDeviceToHost), "read err");

@@ -35,6 +35,24 @@ void cuda_ok(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Makes `d` the current device for one API call and restores the caller's device on return, so a
+// call on one rank's context never leaves another device current behind the caller (e.g. torch).
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int d) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        if (prev_ != d) cuda_ok(cudaSetDevice(d), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        if (prev_ >= 0) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+  private:
+    int prev_ = -1;
+};
+
 std::size_t dtype_size(odc_dtype d) {
     switch (d) {
         case ODC_I64: return 8;
@@ -110,7 +128,7 @@ struct odc_fabric {
                 s.ptr[static_cast<std::size_t>(r)] = base + static_cast<std::int64_t>(k) * stride_bytes + pad;
             }
         }
-        set_device();
+        DeviceGuard dg(dev_id());
         return s;
     }
     // zero every rank's accumulator (a kernel on `device`: the shards may be on peer GPUs)
@@ -123,7 +141,7 @@ struct odc_fabric {
         }
     }
 
-    void set_device() const { cuda_ok(cudaSetDevice(device), "cudaSetDevice"); }
+    int dev_id() const { return device; }
 
     // one copy per simulated rank; the copy kernel's table holds kMaxSeg
     // segments, so any rank count is split into tables of at most kMaxSeg
@@ -246,7 +264,7 @@ odc_status odc_fabric_create_multi(int ranks, std::int64_t elems, odc_dtype dtyp
             f->es = dtype_size(dtype);
             f->device = devices[0];
             for (int r = 0; r < ranks; ++r) f->rank_dev.push_back(devices[r % ndev]);
-            f->set_device();
+            DeviceGuard dg(f->dev_id());
             for (int i = 0; i < ndev; ++i) {  // the primary device's kernels reach every shard
                 if (devices[i] == f->device) continue;
                 int ok = 0;
@@ -266,7 +284,7 @@ odc_status odc_fabric_create_multi(int ranks, std::int64_t elems, odc_dtype dtyp
                 cuda_ok(cudaMalloc(&p, static_cast<std::size_t>(std::max<std::int64_t>(slot_bytes, 16))), "slots");
                 f->slots.push_back(p);
             }
-            f->set_device();
+            cuda_ok(cudaSetDevice(f->dev_id()), "cudaSetDevice");  // the guard above restores the caller's
             cuda_ok(cudaMalloc(&f->stage, static_cast<std::size_t>(elems) * f->es + 16), "stage");
             cuda_ok(cudaMalloc(&f->out, static_cast<std::size_t>(elems) * f->es + 16), "out");
             const std::size_t nn = static_cast<std::size_t>(ranks) * ranks;
@@ -291,7 +309,7 @@ odc_status odc_fabric_create(int ranks, std::int64_t elems, odc_dtype dtype, int
 
 odc_status odc_fabric_destroy(odc_fabric_t f) {
     if (!f) return ODC_OK;
-    cudaSetDevice(f->device);
+    DeviceGuard dg(f->device);
     if (f->stream) cudaStreamSynchronize(f->stream);
     for (auto& kv : f->params)
         for (char* b : kv.second.bases) cudaFree(b);
@@ -315,7 +333,7 @@ odc_status odc_fabric_set_params(odc_fabric_t fh, const char* id, const void* ho
     return odc::guard([&] {
         odc_fabric* f = F(fh);
         if (n != f->elems) throw ParamError("parameter vector length mismatch");
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         auto it = f->params.find(id);
         if (it == f->params.end()) it = f->params.emplace(id, f->alloc_set()).first;
         f->upload(host_full, n);
@@ -337,7 +355,7 @@ odc_status odc_fabric_gather(odc_fabric_t fh, int client, const char* id, void* 
         (void)client;  // read-only fetch: the client rank does not matter (:70)
         auto it = f->params.find(id);
         if (it == f->params.end()) throw StateError(std::string("gather of uninitialized params '") + id + "'");
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         const auto& src = it->second.ptr;
         f->copy_ranks(
             [&](int r, const char*& s, char*& d, std::int64_t& bytes) {
@@ -359,7 +377,7 @@ odc_status odc_fabric_scatter_accumulate(odc_fabric_t fh, int client, const void
         odc_fabric* f = F(fh);
         check_rank(f, client, "client");
         if (n != f->elems) throw ParamError("gradient vector length mismatch");
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         f->upload(host_grad, n);
         if (f->mode == ODC_PUSH_RED) {
             for (int r = 0; r < f->ranks; ++r)  // keep immediate-mode semantics for any staged slot
@@ -388,7 +406,7 @@ odc_status odc_fabric_push_slice(odc_fabric_t fh, int client, int target, std::i
         check_rank(f, client, "client");
         check_rank(f, target, "target");
         if (n < 0) throw ParamError("negative payload length");
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         while (f->occ[f->sidx(target, client)]) f->consume(target, client);
         if (n > f->block)
             throw ProtocolError("payload of " + std::to_string(n) + " elements exceeds the per-client buffer slot of " +
@@ -431,7 +449,7 @@ odc_status odc_fabric_push_slice(odc_fabric_t fh, int client, int target, std::i
 odc_status odc_fabric_finalize(odc_fabric_t fh, void* host_out) {
     return odc::guard([&] {
         odc_fabric* f = F(fh);
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         for (int s = 0; s < f->ranks; ++s)
             for (int c = 0; c < f->ranks; ++c) f->consume(s, c);
         f->take_grads(host_out);
@@ -445,7 +463,7 @@ odc_status odc_fabric_split_stage(odc_fabric_t fh, int from, int target, std::in
         check_rank(f, from, "client");
         check_rank(f, target, "target");
         if (n < 0) throw ParamError("negative payload length");
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         // bounds first (the reference checks before looking at the slot)
         if (n > f->block)
             throw ProtocolError("payload of " + std::to_string(n) + " elements exceeds the per-client buffer slot of " +
@@ -475,7 +493,7 @@ odc_status odc_fabric_consume(odc_fabric_t fh, int server, int client, int* did)
         odc_fabric* f = F(fh);
         check_rank(f, server, "server");
         check_rank(f, client, "client");
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         *did = f->consume(server, client) ? 1 : 0;
         cuda_ok(cudaStreamSynchronize(f->stream), "sync");
     });
@@ -494,7 +512,7 @@ odc_status odc_fabric_any_staged(odc_fabric_t fh, int server, int* any) {
 odc_status odc_fabric_take_grads(odc_fabric_t fh, void* host_out) {
     return odc::guard([&] {
         odc_fabric* f = F(fh);
-        f->set_device();
+        DeviceGuard dg(f->dev_id());
         f->take_grads(host_out);
     });
 }

@@ -233,3 +233,20 @@ def test_fixed_push_range_error_and_underflow_flag():
         with pytest.raises(E.RangeError):
             eng.check()
         eng.close()
+
+
+def test_api_calls_restore_the_callers_device():
+    """Every C-ABI call makes its context's device current only for the call:
+    the caller's current device is unchanged afterwards (several contexts on
+    several devices can be driven from one thread without stray cudaSetDevice)."""
+    n = torch.cuda.device_count()
+    other = n - 1
+    torch.cuda.set_device(0)
+    eng = OdcEngine([1000], device=other)
+    eng.set_params(0, torch.randn(1000, device=f"cuda:{other}"))
+    out = torch.empty(1000, dtype=torch.bfloat16, device=f"cuda:{other}")
+    eng.fetch(0, out)
+    eng.check()
+    assert torch.cuda.current_device() == 0
+    eng.close()
+    assert torch.cuda.current_device() == 0

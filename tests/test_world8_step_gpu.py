@@ -94,7 +94,7 @@ def test_world8_sft_step_matches_world1():
     # world 1, twice: the same 64 samples' microbatches through one engine; the two world-1 runs
     # measure the run-to-run noise floor of bf16 compute with atomic-order fp32 reductions
     def world1():
-        eng = OdcEngine(sizes, push_mode="red")
+        eng = OdcEngine(sizes, push_mode="red", device=0)
         for u, t in enumerate(units(torch.device("cuda", 0))):
             eng.set_params(u, t)
         wk = W.Worker(s, W.OdcComm(eng), "cuda:0", recompute="selective")
