@@ -510,13 +510,21 @@ __device__ __forceinline__ void store_swizzled(char* tile, int r, int c, const u
     }
 }
 
-// warp 0 TMA, warp 1 MMA (warpgroup 0, registers given away with setmaxnreg), warps 4-11 elementwise
-// (two warpgroups, one per 64-column half; each covers the four TMEM lane quadrants)
-constexpr int kBwdThreads = 384;
+// warp 0 TMA, warp 1 MMA (warpgroup 0, registers given away with setmaxnreg), warps 4.. elementwise:
+// kEwWg warpgroups, each owning kCpt of the 128 columns and covering the four TMEM lane quadrants
+#ifndef ODC_BWD_EW_WG
+#define ODC_BWD_EW_WG 2
+#endif
+constexpr int kEwWg = ODC_BWD_EW_WG;
+constexpr int kCpt = 128 / kEwWg;  // columns per elementwise thread
+constexpr int kBwdThreads = 128 + 128 * kEwWg;
+constexpr int kEwRegs = kEwWg == 2 ? 208 : 104;  // setmaxnreg of the elementwise warpgroups
+constexpr int kProdRegs = kEwWg == 2 ? 88 : 56;  // ... and of the TMA / MMA warpgroup
 constexpr int kBwdSmem = kTile * 7 + 1024;  // K, V, Q x2, dO, P, dS
+static_assert(kEwWg == 2 || kEwWg == 4, "2 or 4 elementwise warpgroups");
 
-__device__ __forceinline__ void bar_ew() {  // named barrier over the 8 elementwise warps
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+__device__ __forceinline__ void bar_ew() {  // named barrier over the elementwise warps
+    asm volatile("bar.sync 1, %0;" ::"n"(128 * kEwWg) : "memory");
 }
 __device__ __forceinline__ void tma_reduce_add(const CUtensorMap* map, const void* smem, int c0, int c1) {
     asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
@@ -525,9 +533,10 @@ __device__ __forceinline__ void tma_reduce_add(const CUtensorMap* map, const voi
 }
 // 64 fp32 columns [c0, c0+64) of row r into an fp32 staging tile made of four [128 rows][32 fp32] 128B-swizzled
 // chunks (the box layout of an f32 tensor map with SWIZZLE_128B): conflict-free 16-B stores.
+template <int NCH = 2>
 __device__ __forceinline__ void stage_f32(char* stage, int r, int c0, const unsigned* v) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NCH; ++k) {
         char* row = stage + ((c0 >> 5) + k) * (kTile / 2) + r * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_init(&do_full, 1);
         mbar_init(&do_empty, 1);
         mbar_init(&sdp_full, 1);
-        mbar_init(&s_read, 8);
+        mbar_init(&s_read, 4 * kEwWg);
 #ifdef ODC_ATTN_DEBUG
         if (blockIdx.x == 0)
             printf("bars: kv_full %x q_full %x %x q_empty %x %x do_full %x do_empty %x sdp_full %x s_read %x ds_full %x "
@@ -587,11 +596,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                    su32(&do_full), su32(&do_empty), su32(&sdp_full), su32(&s_read), su32(&ds_full), su32(&dq_full),
                    su32(&dq_read), it.it_end - it.it_begin);
 #endif
-        mbar_init(&p_full, 8);
+        mbar_init(&p_full, 4 * kEwWg);
         mbar_init(&dk_done, 1);
-        mbar_init(&ds_full, 8);
+        mbar_init(&ds_full, 4 * kEwWg);
         mbar_init(&dq_full, 1);
-        mbar_init(&dq_read, 8);
+        mbar_init(&dq_read, 4 * kEwWg);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const unsigned T_DV = 0, T_DK = 128, T_S = 256, T_DP = 384;  // dQ_n reuses T_DP
 
     if (warp < 4) {
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs) : "memory");
       if (warp == 0) {
         if (lane == 0) {  // ---- TMA
             const int k0 = it.seq_start + j * BKV;
@@ -692,13 +701,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     } else {  // ---- elementwise / dQ / dK dV epilogue: row quadrant warp%4, column half
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEwRegs) : "memory");
 #ifdef ODC_ATTN_DEBUG
         if (lane == 0 && blockIdx.x == 0) printf("ew warp %d start\n", warp);
 #endif
         const int quad = warp % 4;
-        const int c0 = ((warp - 4) >> 2) * 64;  // this warp's 64 columns
         const int wg = (warp - 4) >> 2;
+        const int c0 = wg * kCpt;  // this warp's kCpt columns
+        const bool first_half = wg < kEwWg / 2;  // stages its dQ part into sP (else into sdS, after dK)
         const bool lead = (warp & 3) == 0 && lane == 0;  // per warpgroup: issues its half's TMA reductions
         const int r = quad * 32 + lane;  // row: query within tile i (loop) / key within tile j (epilogue)
         const unsigned lane_base = static_cast<unsigned>(quad * 32) << 16;
@@ -723,12 +733,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int lim = q_ok ? min(qi, it.seq_len - 1) - j * BKV - c0 : -1;  // visible keys among our columns
             mbar_wait(&sdp_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lead) TR(5 + 8 * wg, n);
-            unsigned sv[64], dp[64];
-            TM_LD32(tmem + lane_base + T_S + c0, sv);
-            TM_LD32(tmem + lane_base + T_S + c0 + 32, (sv + 32));
-            TM_LD32(tmem + lane_base + T_DP + c0, dp);
-            TM_LD32(tmem + lane_base + T_DP + c0 + 32, (dp + 32));
+            if (lead && wg < 2) TR(5 + 8 * wg, n);
+            unsigned sv[kCpt], dp[kCpt];
+#pragma unroll
+            for (int k = 0; k < kCpt / 32; ++k) {
+                TM_LD32(tmem + lane_base + T_S + c0 + 32 * k, (sv + 32 * k));
+                TM_LD32(tmem + lane_base + T_DP + c0 + 32 * k, (dp + 32 * k));
+            }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -741,10 +752,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // stored and signalled so dV_n runs on the tensor pipe while dS is computed and stored.
             const float2 v_sl2 = make_float2(sl2, sl2), v_nlse = make_float2(-lse2, -lse2);
             const float2 v_sc = make_float2(sc, sc), v_nds = make_float2(-Ds, -Ds);
-            unsigned pk[32];
-            if (lim >= 63) {
+            unsigned pk[kCpt / 2];
+            if (lim >= kCpt - 1) {
 #pragma unroll
-                for (int x = 0; x < 64; x += 2) {
+                for (int x = 0; x < kCpt; x += 2) {
                     const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
                     const float2 pp = make_float2(ex2(t.x), ex2(t.y));
                     sv[x] = __float_as_uint(pp.x);
@@ -753,7 +764,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
             } else {
 #pragma unroll
-                for (int x = 0; x < 64; x += 2) {
+                for (int x = 0; x < kCpt; x += 2) {
                     const float2 t = ffma2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), v_sl2, v_nlse);
                     const float2 pp = make_float2(x > lim ? 0.f : ex2(t.x), x + 1 > lim ? 0.f : ex2(t.y));
                     sv[x] = __float_as_uint(pp.x);
@@ -765,67 +776,67 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // lead committed its own bulk group). P waits for the sP half's read only, and dV_n runs
             // on P while the sdS half still drains into L2
             if (n > 0) {
-                if (lead && wg == 0) {
-                    TR(6, n);
+                if (lead && first_half) {
+                    if (wg == 0) TR(6, n);
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    TR(7, n);
+                    if (wg == 0) TR(7, n);
                 }
                 bar_ew();
             }
-            store_swizzled(sP, r, c0, pk);
-            store_swizzled(sP, r, c0 + 32, pk + 16);
+#pragma unroll
+            for (int k = 0; k < kCpt / 32; ++k) store_swizzled(sP, r, c0 + 32 * k, pk + 16 * k);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full);
-            if (lead) TR(8 + 6 * wg, n);
+            if (lead && wg < 2) TR(8 + 6 * wg, n);
 #pragma unroll
-            for (int x = 0; x < 64; x += 2) {
+            for (int x = 0; x < kCpt; x += 2) {
                 const float2 u = ffma2(make_float2(__uint_as_float(dp[x]), __uint_as_float(dp[x + 1])), v_sc, v_nds);
                 const float2 d = fmul2(make_float2(__uint_as_float(sv[x]), __uint_as_float(sv[x + 1])), u);
                 dp[x / 2] = pack_bf16(d.x, d.y);
             }
             if (n > 0) {
-                if (lead && wg == 1) {
-                    TR(15, n);
+                if (lead && !first_half) {
+                    if (wg == 1) TR(15, n);
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    TR(16, n);
+                    if (wg == 1) TR(16, n);
                 }
                 bar_ew();
             }
-            store_swizzled(sdS, r, c0, dp);
-            store_swizzled(sdS, r, c0 + 32, dp + 16);
+#pragma unroll
+            for (int k = 0; k < kCpt / 32; ++k) store_swizzled(sdS, r, c0 + 32 * k, dp + 16 * k);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&ds_full);
-            if (lead) TR(9 + 8 * wg, n);
+            if (lead && wg < 2) TR(9 + 8 * wg, n);
             // dQ_n (fp32, already scaled) -> smem staging -> TMA reduce-add into the global accumulator,
             // while the MMA warp starts S_{n+1}
             mbar_wait(&dq_full, n & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lead) TR(10 + 8 * wg, n);
-            unsigned v[64];
-            TM_LD32(tmem + lane_base + T_DP + c0, v);
-            TM_LD32(tmem + lane_base + T_DP + c0 + 32, (v + 32));
+            if (lead && wg < 2) TR(10 + 8 * wg, n);
+            unsigned v[kCpt];
+#pragma unroll
+            for (int k = 0; k < kCpt / 32; ++k) TM_LD32(tmem + lane_base + T_DP + c0 + 32 * k, (v + 32 * k));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&dq_read);
             // warpgroup 0's half goes to sP (free: dV_n read P before dQ_n), warpgroup 1's to sdS once
             // dK_n has read dS
-            if (wg == 1) mbar_wait(&dk_done, n & 1);
-            if (lead) TR(11 + 8 * wg, n);
-            stage_f32(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
+            if (!first_half) mbar_wait(&dk_done, n & 1);
+            if (lead && wg < 2) TR(11 + 8 * wg, n);
+            stage_f32<kCpt / 32>(stage, r, c0, v);  // rows past the sequence end hold exact zeros (P = dS = 0)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
             if (lead) {
                 const int row0 = it.seq_start + i * BQ;
 #pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    tma_reduce_add(&map_dq, stage + (2 * wg + k) * (kTile / 2), h * HD + c0 + 32 * k, row0);
+                for (int k = 0; k < kCpt / 32; ++k)
+                    tma_reduce_add(&map_dq, stage + (c0 / 32 + k) * (kTile / 2), h * HD + c0 + 32 * k, row0);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                TR(12 + 8 * wg, n);
+                if (wg < 2) TR(12 + 8 * wg, n);
             }
         }
         // dK, dV of the key tile (every MMA done once the last dK finished) -> staging -> TMA reduce-add
@@ -836,15 +847,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         char* st_dv = sP;  // [sP, sdS]
         char* st_dk = sQ0;  // both Q buffers: Q is no longer read
         {
-            unsigned v[64];
-            TM_LD32(tmem + lane_base + T_DV + c0, v);
-            TM_LD32(tmem + lane_base + T_DV + c0 + 32, (v + 32));
+            unsigned v[kCpt];
+#pragma unroll
+            for (int k = 0; k < kCpt / 32; ++k) TM_LD32(tmem + lane_base + T_DV + c0 + 32 * k, (v + 32 * k));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            stage_f32(st_dv, r, c0, v);
-            TM_LD32(tmem + lane_base + T_DK + c0, v);
-            TM_LD32(tmem + lane_base + T_DK + c0 + 32, (v + 32));
+            stage_f32<kCpt / 32>(st_dv, r, c0, v);
+#pragma unroll
+            for (int k = 0; k < kCpt / 32; ++k) TM_LD32(tmem + lane_base + T_DK + c0 + 32 * k, (v + 32 * k));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            stage_f32(st_dk, r, c0, v);
+            stage_f32<kCpt / 32>(st_dk, r, c0, v);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_ew();
